@@ -1,0 +1,204 @@
+"""Pins of the oracle's tree algorithms (oracle/tree.py) against what the paper
+and plain mathematics fix: closed forms, the Fig. 3 caption, App. A.1 sizes,
+brute force on small inputs.  CPU only."""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import tree as T
+from synth import gen
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------------ Eq. 1
+def test_eq1_closed_forms():
+    # root = empty product = 1; one step 0.5 * 0.4 = 0.2
+    cu = T.cumulative_scores([-1, 0, 1], [1.0, 0.5, 0.4])
+    assert cu[0] == np.float32(1.0)
+    assert cu[1] == np.float32(0.5)
+    assert cu[2] == np.float32(np.float32(0.5) * np.float32(0.4))
+    assert abs(float(cu[2]) - 0.2) < 1e-7
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_eq1_equals_path_product_walk(seed):
+    t = gen.random_tree(seed, 40, 8, 50, 3)
+    cu = T.cumulative_scores(t["parent"], t["own"])
+    for i in range(40):
+        # brute force: walk to the root collecting own scores, multiply root->node
+        path, p = [], i
+        while p >= 0:
+            path.append(p)
+            p = t["parent"][p]
+        prod = np.float32(1.0)
+        for j in reversed(path[:-1]):
+            prod = np.float32(prod * np.float32(t["own"][j]))
+        assert prod == cu[i]
+        assert abs(float(cu[i]) - float(np.prod(np.float64(t["own"][path[:-1]])))) < 1e-5
+        if t["parent"][i] >= 0:  # scores never increase down the tree
+            assert cu[i] <= cu[t["parent"][i]]
+
+
+# ------------------------------------------------------------------ order
+@pytest.mark.parametrize("seed", range(20))
+def test_order_is_bruteforce_sort_and_topological(seed):
+    t = gen.random_tree(100 + seed, 60, 6, 40, 1)
+    cu = T.cumulative_scores(t["parent"], t["own"])
+    ids = np.arange(60)
+    order = T.score_order(cu, ids)
+    # brute force: repeatedly extract the max (cu, then smallest id)
+    rest, bf = set(range(60)), []
+    while rest:
+        best = None
+        for i in rest:
+            if best is None or cu[i] > cu[best] or (cu[i] == cu[best] and i < best):
+                best = i
+        bf.append(best)
+        rest.remove(best)
+    assert order == bf
+    pos = {v: k for k, v in enumerate(order)}
+    for i in range(1, 60):  # parent before child
+        assert pos[t["parent"][i]] < pos[i]
+    # every prefix is ancestor-closed, so every top-L is a connected tree
+    for L in range(1, 61):
+        keep = set(T.top_L(order, L))
+        assert all(t["parent"][i] in keep for i in keep if i != 0)
+
+
+def test_planted_tree_meets_target_order():
+    for seed in range(10):
+        stream = list(range(10, 20))
+        t = gen.planted_tree(seed, 64, 6, stream, (0, 2, 5, 17, 21), 1000)
+        cu = T.cumulative_scores(t["parent"], t["own"])
+        assert [int(i) for i in T.score_order(cu, np.arange(64))] == list(t["order"])
+
+
+def test_segments_appendix_a1():
+    g = _gold("appendix_a1_segments.json")
+    for c in g["cases"]:
+        b = T.segment_bounds(c["n"], c["l_max"])
+        assert [e - s for s, e in b] == c["lengths"]
+        assert b[0][0] == 0 and b[-1][1] == c["n"]
+        assert all(b[k][1] == b[k + 1][0] for k in range(len(b) - 1))
+
+
+# ------------------------------------------------------------------ masks
+def test_mask_special_cases():
+    # chain -> lower-triangular; root with two children -> siblings invisible
+    assert T.ancestors_or_self([-1, 0, 1]) == [{0}, {0, 1}, {0, 1, 2}]
+    assert T.ancestors_or_self([-1, 0, 0]) == [{0}, {0, 1}, {0, 2}]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_mask_equals_transitive_closure(seed):
+    t = gen.random_tree(500 + seed, 30, 7, 30, 0)
+    n = 30
+    A = np.zeros((n, n), bool)  # A[i, j]: j is the parent of i
+    for i in range(1, n):
+        A[i, t["parent"][i]] = True
+    R = np.eye(n, dtype=bool)
+    for _ in range(n):  # reflexive-transitive closure by repeated squaring-ish
+        R = R | (R.astype(np.int32) @ A.astype(np.int32) > 0)
+    anc = T.ancestors_or_self(list(t["parent"]))
+    for i in range(n):
+        assert anc[i] == set(np.nonzero(R[i])[0].tolist())
+    d = T.depth_of(list(t["parent"]))
+    assert all(len(anc[i]) == d[i] + 1 for i in range(n))
+
+
+# ------------------------------------------------------------------ accept
+def test_accept_zero_acceptance_and_perfect_alignment():
+    par = [-1, 0, 1, 2]
+    tok = [5, 6, 7, 8]
+    # argmax at root not among its children: S_acc = [root] (R2), exit
+    r = T.accept_walk(par, tok, [9, 0, 0, 0], [True] * 4)
+    assert r == dict(progress=1, acc=[0], x_new=9, n_new=-1, cont=0)
+    # perfectly aligned chain: accept everything, bonus token after the leaf
+    r = T.accept_walk(par, tok, [6, 7, 8, 3], [True] * 4)
+    assert r["acc"] == [0, 1, 2, 3] and r["x_new"] == 3 and not r["cont"]
+    # unverified child matching the argmax: stop before it, continue (R3, Eq. 2)
+    r = T.accept_walk(par, tok, [6, 7, 0, 0], [True, True, False, False])
+    assert r["acc"] == [0, 1] and r["n_new"] == 2 and r["cont"] == 1
+    # root unverified: no progress (R23)
+    assert T.accept_walk(par, tok, [6, 7, 8, 3], [False] * 4) == dict(progress=0)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_accept_matches_bruteforce_path_search(seed):
+    rng = gen.Rng(seed)
+    t = gen.random_tree(900 + seed, 25, 5, 6, 0)
+    par, tok = list(t["parent"]), list(t["token"])
+    am = [rng.below(6) for _ in range(25)]
+    ver = [True] * 25
+    r = T.accept_walk(par, tok, am, ver)
+    # brute force: the longest root path whose every step follows the argmax;
+    # Eq. 2 by a linear scan over all node paths
+    paths = {}
+    for i in range(25):
+        p, pth = i, []
+        while p >= 0:
+            pth.append(tok[p])
+            p = par[p]
+        paths[i] = tuple(reversed(pth))
+    best = [0]
+    for i in range(25):
+        pth = [i]
+        p = par[i]
+        while p >= 0:
+            pth.append(p)
+            p = par[p]
+        pth.reverse()
+        if all(tok[pth[k + 1]] == am[pth[k]] for k in range(len(pth) - 1)) and len(pth) > len(best):
+            best = pth
+    assert r["acc"] == best
+    want = paths[best[-1]] + (am[best[-1]],)
+    found = [i for i in range(25) if paths[i] == want]
+    assert r["cont"] == int(bool(found)) and (r["n_new"] == (found[0] if found else -1))
+
+
+# ------------------------------------------------------------------ prune
+def test_fig3_prune_vector():
+    g = _gold("fig3_pruning.json")
+    par = g["parent_s"]
+    anc = T.ancestors_or_self(par)
+    i_acc, i_pr, i_ret = T.prune_sets(g["acc"], g["n_new"], anc, len(par))
+    assert i_acc == g["I_acc"] and i_pr == g["I_pr"] and i_ret == g["I_retain"]
+    assert T.rank_map(i_ret) == {int(k): v for k, v in g["rank_map"].items()}
+    assert T.segment_bounds(len(par), g["l_max"]) == [tuple(s) for s in g["segments"]]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_prune_equals_path_prefix_bruteforce(seed):
+    rng = gen.Rng(7 * seed + 1)
+    t = gen.random_tree(300 + seed, 40, 6, 5, 2)
+    par, tok = list(t["parent"]), list(t["token"])
+    am = [rng.below(5) for _ in range(40)]
+    r = T.accept_walk(par, tok, am, [True] * 40)
+    anc = T.ancestors_or_self(par)
+    i_acc, i_pr, i_ret = T.prune_sets(r["acc"], r["n_new"], anc, 40)
+    # brute force: keep nodes whose token path has S_acc||x_new as prefix
+    def path(i):
+        out = []
+        while i >= 0:
+            out.append(tok[i])
+            i = par[i]
+        return out[::-1]
+    pre = [tok[i] for i in r["acc"]] + [r["x_new"]]
+    bf = [i for i in range(40) if path(i)[:len(pre)] == pre]
+    assert i_pr == (bf if r["cont"] else [])
+    # causality: retained entries keep their retained ancestors before them
+    for i in i_pr:
+        assert all(a in i_pr for a in anc[i] if a >= r["n_new"] and a in anc[i] and r["n_new"] in anc[a])
+    # accepted indices all precede retained draft indices (so accepted rows land
+    # at l_glo..l_glo'-1 after compaction, SURVEY §8(c) "Compaction")
+    if i_pr:
+        assert max(i_acc) < min(i_pr)
