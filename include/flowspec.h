@@ -1,0 +1,216 @@
+/*
+ * flowspec.h — C-ABI of the B200-native FlowSpec pipelined tree-verification
+ * hot path (arXiv 2507.02620).  libflowspec.so, sm_100a.
+ *
+ * Citations: P:NNN = /root/reference/PAPER.md line NNN (section / equation);
+ * R# = reading of DESIGN.md.
+ *
+ * Execution model: SPMD, one process per GPU, rank p = pipeline stage p
+ * ("the base LLM is partitioned into N consecutive layer blocks").
+ * Every rank makes the same sequence of calls with identical host inputs; the
+ * draft tree is replicated on every rank ("all stages need to perform pruning
+ * over its local replicas of T").  Calls marked COLLECTIVE communicate
+ * over NCCL (NVLink); all other calls are local.
+ *
+ * Conventions
+ *  - Return: FS_OK (0) or a negative FS_E* code; no exception crosses the ABI.
+ *    A failing call leaves the state unchanged, except FS_ECUDA/FS_ENCCL which
+ *    poison the context (every later call returns FS_EPOISONED).
+ *  - Host arrays passed in are caller-owned and copied before return.  Output
+ *    structs are caller-owned, fixed capacity.
+ *  - Device memory comes only from the caller's arena (fs_config.arena, e.g.
+ *    a torch.empty(uint8) tensor); the library allocates no device memory.
+ *  - Work is issued on fs_config.stream; calls that return results to the host
+ *    synchronise that stream before returning.
+ *  - A context is single-owner and not thread-safe.
+ */
+#ifndef FLOWSPEC_H
+#define FLOWSPEC_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FS_OK 0
+#define FS_EINVAL (-1)     /* bad argument / malformed tree */
+#define FS_ENOMEM (-2)     /* arena too small */
+#define FS_ESTATE (-3)     /* call not valid in the current state */
+#define FS_ECAPACITY (-4)  /* max_ctx / max_live / max_seg exceeded */
+#define FS_ECUDA (-5)      /* CUDA error: context poisoned */
+#define FS_ENCCL (-6)      /* NCCL error: context poisoned */
+#define FS_EPOISONED (-7)  /* an earlier CUDA/NCCL error poisoned the context */
+
+#define FS_MAX_LIVE 512    /* hard cap on live draft nodes (ancestor bitsets) */
+#define FS_MAX_SEG 64      /* hard cap on rows per segment */
+#define FS_MAX_STAGES 8
+
+typedef struct fs_config {
+  /* model shape (LLaMA2 / Qwen2 decoder, App. B.1; R19) */
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  int32_t qkv_bias;         /* 1: q/k/v projections carry a bias (Qwen2) */
+  int32_t bf16;             /* 1: bf16 weights/activations, fp32 accumulate and
+                               residual (precision contract R18); 0: fp32
+                               everywhere, no TF32 */
+  double rms_eps, rope_theta;
+  /* pipeline */
+  int32_t n_stages;         /* 1..FS_MAX_STAGES */
+  int32_t rank;             /* this process' stage, 0..n_stages-1 */
+  const int32_t* layers_per_stage; /* n_stages entries summing to n_layers, or
+                               NULL = byte-balanced consecutive blocks (head
+                               bytes counted on the last stage) */
+  /* capacities */
+  int32_t max_ctx;          /* KV slots (context + live drafts) */
+  int32_t max_live;         /* live draft nodes, <= FS_MAX_LIVE, multiple of 32 */
+  int32_t max_seg;          /* rows per segment / prefill chunk, <= FS_MAX_SEG */
+  /* plumbing (PyTorch: device memory, stream, process group bootstrap) */
+  int32_t device;
+  void* arena;              /* device pointer, >= fs_arena_bytes(cfg) bytes, 256-B aligned */
+  size_t arena_bytes;
+  void* stream;             /* cudaStream_t the library issues all work on */
+  const uint8_t* nccl_id;   /* 128-byte ncclUniqueId from rank 0 (n_stages > 1) */
+} fs_config;
+
+typedef struct fs_ctx fs_ctx;
+
+/* Bytes of device arena the configuration needs (weights of this rank's layer
+ * block, KV cache, activations, tree state, workspaces).  0 if cfg invalid. */
+size_t fs_arena_bytes(const fs_config* cfg);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast it). */
+int fs_nccl_unique_id(uint8_t* out);
+
+/* Create a context.  Validates cfg (FS_EINVAL), checks the arena
+ * (FS_ENOMEM), joins the NCCL communicator when n_stages > 1. */
+int fs_init(const fs_config* cfg, fs_ctx** out);
+
+/* Fill this rank's weights (its layer block; embedding on stage 0; final norm
+ * and head on the last stage) on the device with the counter-based generator
+ * of DESIGN.md "Input recipe": uniform, std sigma, bf16 RNE.
+ * No host buffers.  FS_ESTATE if called twice. */
+int fs_load_random_weights(fs_ctx* ctx, uint64_t seed);
+
+#define FS_PREFILL 0  /* chain-mask passes of <= max_seg rows (P:214 chunked prefill) */
+#define FS_SYNTH_KV 1 /* slots [0,n-1) synthetic K/V, last token real (configs 4-5) */
+/* COLLECTIVE.  Build the prefix KV cache and the first sampled token:
+ * l_glo = n, *x_new_out = argmax of the last prefix token's logits
+ * ("compute the initial KV cache and generate the first sampled token
+ * x_new").  Drops any live round.  FS_EINVAL: n < 1, bad token, bad mode;
+ * FS_ECAPACITY: n + max_live > max_ctx. */
+int fs_set_prefix(fs_ctx* ctx, const int32_t* tok, int32_t n, int32_t mode,
+                  uint64_t kv_seed, int32_t* x_new_out);
+
+#define FS_NEW_ROUND 1 /* draft initialization step */
+#define FS_APPEND 2    /* expansion: S <- S || S_app */
+typedef struct fs_submit_out {
+  int32_t n;                     /* nodes added (after optional top-L) */
+  int32_t s_base;                /* S index of the first added node */
+  int32_t order[FS_MAX_LIVE];    /* node ids of the batch in S order */
+  int32_t n_segs;                /* segments enqueued */
+  int32_t seg_begin[FS_MAX_LIVE + 1]; /* S-index bounds, n_segs+1 entries */
+  int32_t seg_id0;               /* id of the first enqueued segment */
+} fs_submit_out;
+/* Local.  Submit a draft tree (NEW_ROUND) or an appended batch (APPEND) and
+ * enqueue it as segments:
+ *   Eq. 1: cu = own * cu(parent), fp32, root cu = 1 (R11);
+ *   score order: cu descending, node id ascending (R10); optional
+ *   top-L_top (L_top = 0: keep all); S-order prefixes are ancestor-closed
+ *   (P:284);  segments: consecutive slices of <= L_max (R12); an
+ *   appended batch forms its own segments;  positions pos = l_glo + depth
+ *   (R4) and ancestor-or-self bitsets.
+ * parent[i]: node id of the parent (NEW_ROUND: ids are 0..n-1, node 0 is the
+ * root with parent -1 and token == current x_new; APPEND: ids continue the
+ * round's sequence, parents are live ids or earlier ids of the batch);
+ * token[i] vocabulary id; own[i] draft score in (0, 1].
+ * FS_EINVAL: n < 1, L_max < 1 or > max_seg, L_top < 0, parent[i] >= id(i),
+ * unknown/pruned parent, duplicate sibling token, own outside (0,1], bad
+ * token, root token != x_new.  FS_ESTATE: APPEND without a live round,
+ * NEW_ROUND while a round is live.  FS_ECAPACITY: live nodes > max_live. */
+int fs_submit_segment(fs_ctx* ctx, int32_t flags, const int32_t* parent,
+                      const int32_t* token, const float* own, int32_t n,
+                      int32_t L_top, int32_t L_max, fs_submit_out* out);
+
+typedef struct fs_step_out {
+  int32_t seg_id;            /* segment that left the last stage, -1 if none */
+  int32_t s_begin, n_rows;   /* its S range (n_rows 0: pruned-empty bubble) */
+  int32_t node[FS_MAX_SEG];  /* node ids of the rows */
+  int32_t am[FS_MAX_SEG];    /* greedy target token (argmax, lowest id on ties) */
+  float margin[FS_MAX_SEG];  /* top-1 minus top-2 logit */
+} fs_step_out;
+/* COLLECTIVE.  One pipeline tick (P:228 step-wise pipelined verification):
+ * stage 0 takes the next queued segment; every stage runs its in-flight
+ * segment through its layer block (tree-masked attention over the prefix KV
+ * plus ancestor drafts), hidden rows move p -> p+1 (NCCL send/recv);
+ * the last stage computes final norm + head + argmax/top-2 (R7) and the
+ * per-row results are broadcast to every rank.  Every rank gets the same
+ * *out. */
+int fs_verify_step(fs_ctx* ctx, fs_step_out* out);
+
+/* Optional parity readback: device buffer of rows_cap x vocab fp32 where the
+ * last stage writes the logits of each verified segment (NULL disables). */
+int fs_set_logits_buffer(fs_ctx* ctx, float* dev_logits, int32_t rows_cap);
+
+typedef struct fs_accept_out {
+  int32_t progress;          /* 0: the current root is not verified yet (R23) */
+  int32_t n_acc;             /* |S_acc|, root included (R2) */
+  int32_t acc_ids[FS_MAX_LIVE];
+  int32_t acc_tokens[FS_MAX_LIVE];
+  int32_t x_new;             /* token sampled after S_acc */
+  int32_t n_new;             /* node id with path S_acc||x_new, or -1 */
+  int32_t cont;              /* Eq. 2 continuous condition */
+  int32_t n_flagged;         /* walked nodes with top-2 margin < 1e-2 */
+  int32_t flagged_ids[FS_MAX_LIVE];
+} fs_accept_out;
+/* Local (deterministic on replicated state, so every rank computes the same
+ * record).  Greedy acceptance + Eq. 2 over all verified nodes (R1,
+ * R3): from the root, descend while the child carrying the argmax exists and
+ * is verified. */
+int fs_accept(fs_ctx* ctx, fs_accept_out* out);
+
+/* Local.  Apply a decision (normally fs_accept's; the parity harness may pass
+ * the oracle's after a flagged near-tie):
+ *  cont = 1: tree pruning: I_retain = I_acc ∪ I_pr; each stage keeps
+ *    retained draft KV rows (I_incache) by a stable
+ *    stream-compaction gather slot l_glo+i -> l_glo+rank(i), prunes its
+ *    in-flight hidden rows and queued segments (I_local),
+ *    re-roots S at n_new, then l_glo += |S_acc|.
+ *  cont = 0: round exit: S_acc becomes context, everything else drops.
+ * FS_ESTATE: no live round, progress = 0, ids not live, S_acc not a root path,
+ * n_new not a child of the last accepted node. */
+int fs_prune_and_compact(fs_ctx* ctx, const fs_accept_out* decision);
+
+/* ---- parity / introspection ---- */
+typedef struct fs_state {
+  int32_t l_glo, x_new, live, n_live, next_id;
+  int32_t n_stages, rank, layer_begin, layer_end;
+  int32_t n_cached[FS_MAX_STAGES];   /* per stage: S indices < n_cached have KV */
+  int32_t layers_per_stage[FS_MAX_STAGES];
+  int32_t n_queue;                   /* queued (undispatched) segments */
+  int32_t queue[FS_MAX_LIVE][3];     /* {seg_id, s_begin, s_end} */
+  int32_t inflight[FS_MAX_STAGES][3];/* segment each stage runs next tick, seg_id -1 = none */
+  uint64_t launches;                 /* kernels this rank launched so far */
+} fs_state;
+#define FS_Q_STATE 0   /* fs_state */
+#define FS_Q_NODE 1    /* int32[n_live] node ids in S order */
+#define FS_Q_TOKEN 2   /* int32[n_live] */
+#define FS_Q_PARENT 3  /* int32[n_live] parent S index (-1 root) */
+#define FS_Q_POS 4     /* int32[n_live] l_glo + depth */
+#define FS_Q_ANC 5     /* uint32[n_live][max_live/32] ancestor-or-self bitsets */
+#define FS_Q_CU 6      /* float[n_live] cumulative scores relative to the root */
+#define FS_Q_RETAIN 7  /* uint32[max_live/32] I_retain of the last prune */
+/* Copy item `what` into buf (bytes capacity); *needed receives the size. */
+int fs_query(fs_ctx* ctx, int32_t what, void* buf, size_t bytes, size_t* needed);
+
+/* Read one K (which=0) or V (which=1) row (head_dim values as fp32) of a
+ * layer owned by this rank.  FS_EINVAL otherwise. */
+int fs_read_kv(fs_ctx* ctx, int32_t layer, int32_t which, int32_t kv_head,
+               int32_t slot, float* out);
+
+void fs_destroy(fs_ctx* ctx);
+const char* fs_last_error(const fs_ctx* ctx);
+const char* fs_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -5,11 +5,11 @@
  * Arithmetic is fp64 throughout; values are rounded only where the precision
  * contract stores them:
  *   residual x ............ fp32
- *   RMSNorm output ........ bf16 (fp32 config: fp32)
- *   q, k, v (after bias+RoPE) bf16
- *   attention output ...... bf16
- *   silu(g)*u ............. bf16
+ *   q, k, v (after bias+RoPE) bf16 (K/V cache storage)
+ *   RMSNorm output, attention output, silu(g)*u (the GEMM inputs):
+ *                           fp32 carried as bf16 hi + bf16 lo
  *   logits ................ fp32
+ * (fp32 config: fp32 everywhere)
  * Compile with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
  *
  * Paper passages followed:
@@ -328,9 +328,20 @@ int32_t fso_kv_synth(fso_kv* kv, int32_t n, uint64_t kv_seed) {
 
 /* ----------------------------------------------------------------- forward */
 static float store_act(const fso_cfg* c, double v) {
-  /* activation storage: fp32, then bf16 under the bf16 contract */
+  /* q/k/v storage: fp32, then bf16 under the bf16 contract */
   float f = (float)v;
   return c->bf16 ? fso_round_bf16(f) : f;
+}
+
+/* GEMM-input activations (RMSNorm outputs, attention output, silu*up): fp32,
+ * carried under the bf16 contract as a pair of bf16 values hi + lo with
+ * hi = bf16(f), lo = bf16(f - hi)  (R18) */
+static double store_act2(const fso_cfg* c, double v) {
+  float f = (float)v;
+  if (!c->bf16) return f;
+  float hi = fso_round_bf16(f);
+  float lo = fso_round_bf16(f - hi);
+  return (double)hi + (double)lo;
 }
 
 /* y[m] = round(x[m] * rsqrt(mean(x[m]^2) + eps) * g)   (RMSNorm, LLaMA) */
@@ -345,7 +356,7 @@ static void rmsnorm(fso_model* m, int32_t layer, int32_t which, int32_t n_rows,
     for (int32_t k = 0; k < d; k++) ss += (double)x[(int64_t)r * d + k] * (double)x[(int64_t)r * d + k];
     double inv = 1.0 / sqrt(ss / d + c->rms_eps);
     for (int32_t k = 0; k < d; k++)
-      y[(int64_t)r * d + k] = store_act(c, (double)x[(int64_t)r * d + k] * inv * (double)g[k]);
+      y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * inv * (double)g[k]);
   }
   free(g);
 }
@@ -492,7 +503,7 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
           double p = s[j] / den;
           for (int32_t t = 0; t < hd; t++) oh[t] += p * kv_load(kv, vb + t);
         }
-        for (int32_t t = 0; t < hd; t++) oh[t] = store_act(c, oh[t]);
+        for (int32_t t = 0; t < hd; t++) oh[t] = store_act2(c, oh[t]);
         free(s);
       }
     linear(m, l, FSO_O, n_rows, att, o);
@@ -504,7 +515,7 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
     linear(m, l, FSO_UP, n_rows, y, u);
     for (int64_t i = 0; i < (int64_t)n_rows * c->ffn; i++) {
       double gv = g[i];
-      g[i] = store_act(c, gv / (1.0 + exp(-gv)) * u[i]);
+      g[i] = store_act2(c, gv / (1.0 + exp(-gv)) * u[i]);
     }
     linear(m, l, FSO_DOWN, n_rows, g, o);
     for (int64_t i = 0; i < (int64_t)n_rows * d; i++) x[i] = (float)((double)x[i] + o[i]);

@@ -1,0 +1,1214 @@
+// api.cu — the fs_* C-ABI (include/flowspec.h): per-rank stage runtime, tick
+// scheduler, NCCL stage transport and the launch sequences of the kernels.
+//
+// Host code here does bookkeeping only (which segment each stage runs this
+// tick, arena carving, argument marshalling); every step of the path —
+// tree metadata, decoder layers, argmax, acceptance, pruning, compaction —
+// runs in the kernels of k_*.cuh.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "../../include/flowspec.h"
+#include "common.cuh"
+#include "k_fwd.cuh"
+#include "k_gemm.cuh"
+#include "k_gen.cuh"
+#include "k_tree.cuh"
+#include "state.cuh"
+
+using namespace fs;
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+struct Seg {
+  int id = -1, b = 0, e = 0;
+  bool valid() const { return id >= 0; }
+  int n() const { return e - b; }
+};
+
+struct GemmOp {
+  CUtensorMap ta, tb;
+  GemmShape sh;
+  int grid = 0;
+  bool ok = false;
+};
+
+struct LayerW {
+  void *wqkv = nullptr, *bqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
+  void *g1 = nullptr, *g2 = nullptr;
+  GemmOp qkv, o, gu, dn;
+};
+
+}  // namespace
+
+struct fs_ctx {
+  fs_config cfg;
+  int lps[FS_MAX_STAGES];
+  int P = 1, rank = 0, L0 = 0, L1 = 0, nl = 0;
+  bool first = true, last = true, bf = true;
+  int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  // arena
+  char* base = nullptr;
+  size_t off = 0, cap = 0;
+  // weights
+  std::vector<LayerW> lw;
+  void *emb = nullptr, *wh = nullptr, *gf = nullptr;
+  GemmOp head;
+  // kv / rope
+  char* kv = nullptr;
+  size_t kv_plane_elems = 0;  // Hkv * max_ctx * hd
+  float2* rope = nullptr;
+  // activations
+  float *x = nullptr, *hin = nullptr, *yf = nullptr;
+  void *y = nullptr, *q = nullptr, *att = nullptr, *act = nullptr;
+  float *gws = nullptr;
+  int* gcnt = nullptr;
+  Top2* head_part = nullptr;
+  RowResult* res = nullptr;
+  int32_t* out_node = nullptr;
+  float *aws_o = nullptr, *aws_ml = nullptr;
+  int att_chunk_cap = 0;
+  size_t gws_floats = 0;
+  // tree
+  TreeDev tree;
+  SubmitIn* d_sub = nullptr;
+  DecisionIn* d_dec = nullptr;
+  TreeRecord* d_rec = nullptr;
+  TickRows* d_rows = nullptr;
+  // pinned host staging
+  SubmitIn* h_sub = nullptr;
+  DecisionIn* h_dec = nullptr;
+  TreeRecord* h_rec = nullptr;
+  TickRows* h_rows = nullptr;
+  RowResult* h_res = nullptr;
+  int32_t* h_node = nullptr;
+  // schedule (replicated on every rank)
+  int l_glo = 0, x_new = -1, live = 0, n_live = 0, next_id = 0, seg_counter = 0;
+  std::deque<Seg> queue;
+  Seg slot[FS_MAX_STAGES];
+  int n_cached[FS_MAX_STAGES] = {0};
+  bool weights = false, poisoned = false, prefixed = false;
+  std::string err;
+  uint64_t launches = 0;
+  float* logits_buf = nullptr;
+  int logits_cap = 0;
+};
+
+namespace {
+
+
+int fail(fs_ctx* c, int code, const char* msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK_CUDA(c, expr)                                                    \
+  do {                                                                      \
+    cudaError_t e_ = (expr);                                                \
+    if (e_ != cudaSuccess) {                                                \
+      (c)->poisoned = true;                                                 \
+      (c)->err = std::string(#expr) + ": " + cudaGetErrorString(e_);        \
+      return FS_ECUDA;                                                      \
+    }                                                                       \
+  } while (0)
+#define CK_NCCL(c, expr)                                                    \
+  do {                                                                      \
+    ncclResult_t r_ = (expr);                                               \
+    if (r_ != ncclSuccess) {                                                \
+      (c)->poisoned = true;                                                 \
+      (c)->err = std::string(#expr) + ": " + ncclGetErrorString(r_);        \
+      return FS_ENCCL;                                                      \
+    }                                                                       \
+  } while (0)
+#define CK_LAUNCH(c)                                                        \
+  do {                                                                      \
+    (c)->launches++;                                                        \
+    cudaError_t e_ = cudaGetLastError();                                    \
+    if (e_ != cudaSuccess) {                                                \
+      (c)->poisoned = true;                                                 \
+      (c)->err = std::string("launch: ") + cudaGetErrorString(e_);          \
+      return FS_ECUDA;                                                      \
+    }                                                                       \
+  } while (0)
+
+// ---------------------------------------------------------------- validation
+bool cfg_valid(const fs_config* c, std::string* why) {
+  auto bad = [&](const char* s) {
+    if (why) *why = s;
+    return false;
+  };
+  if (!c) return bad("null cfg");
+  if (c->n_layers < 1 || c->d_model < 1 || c->n_heads < 1 || c->n_kv_heads < 1 ||
+      c->head_dim < 2 || c->ffn < 1 || c->vocab < 2)
+    return bad("bad model shape");
+  if (c->n_heads % c->n_kv_heads) return bad("n_heads % n_kv_heads");
+  if (c->head_dim % 2) return bad("odd head_dim");
+  if (c->ffn % 64) return bad("ffn must be a multiple of 64 (interleaved gate/up tiles)");
+  if (c->bf16) {
+    if (c->head_dim != 128) return bad("bf16 path needs head_dim 128");
+    if (c->d_model % 64 || (c->n_heads * c->head_dim) % 64) return bad("K dims must be multiples of 64");
+  } else {
+    if (c->head_dim * 4 % 16) return bad("fp32 head_dim must be a multiple of 4");
+  }
+  if (c->n_stages < 1 || c->n_stages > FS_MAX_STAGES) return bad("n_stages");
+  if (c->rank < 0 || c->rank >= c->n_stages) return bad("rank");
+  if (c->n_stages > c->n_layers) return bad("more stages than layers");
+  if (c->layers_per_stage) {
+    int s = 0;
+    for (int p = 0; p < c->n_stages; p++) {
+      if (c->layers_per_stage[p] < 1) return bad("layers_per_stage entry < 1");
+      s += c->layers_per_stage[p];
+    }
+    if (s != c->n_layers) return bad("layers_per_stage does not sum to n_layers");
+  }
+  if (c->max_live < 32 || c->max_live > FS_MAX_LIVE || c->max_live % 32) return bad("max_live");
+  if (c->max_seg < 1 || c->max_seg > FS_MAX_SEG) return bad("max_seg");
+  if (c->max_ctx < c->max_live + 2) return bad("max_ctx");
+  if (c->rms_eps <= 0 || c->rope_theta <= 0) return bad("eps/theta");
+  return true;
+}
+
+// byte-balanced consecutive layer blocks; the head (V*d) counts on the last stage
+void balance(const fs_config* c, int* out) {
+  const int P = c->n_stages, L = c->n_layers;
+  if (c->layers_per_stage) {
+    for (int p = 0; p < P; p++) out[p] = c->layers_per_stage[p];
+    return;
+  }
+  const double layer = (double)c->d_model * (c->n_heads + 2 * c->n_kv_heads) * c->head_dim +
+                       (double)c->n_heads * c->head_dim * c->d_model + 3.0 * c->d_model * c->ffn;
+  const double head = (double)c->vocab * c->d_model / layer;
+  int last = (int)std::lround((L + head) / P - head);
+  last = std::max(1, std::min(last, L - (P - 1)));
+  if (P == 1) last = L;
+  const int rest = L - last;
+  for (int p = 0; p < P - 1; p++) out[p] = rest / (P - 1) + (p < rest % (P - 1) ? 1 : 0);
+  out[P - 1] = last;
+}
+
+int npad_of(int max_seg) { return max_seg <= 16 ? 16 : (max_seg <= 32 ? 32 : 64); }
+
+// ---------------------------------------------------------------- arena
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+void plan_gemm(GemmOp& g, int n_out, int K, int n_sms) {
+  g.sh.n_out = n_out;
+  g.sh.K = K;
+  g.sh.kb_total = K / 64;
+  g.sh.n_tiles = (n_out + 127) / 128;
+  g.sh.units = g.sh.n_tiles * g.sh.kb_total;
+  g.grid = std::min(n_sms, g.sh.units);
+  int mc = 1;
+  const int U = g.sh.units, G = g.grid, KB = g.sh.kb_total;
+  auto cta = [&](int u) { return (int)(((long long)(u + 1) * G + U - 1) / U) - 1; };
+  for (int t = 0; t < g.sh.n_tiles; t++) mc = std::max(mc, cta((t + 1) * KB - 1) - cta(t * KB) + 1);
+  g.sh.max_contrib = mc;
+}
+
+// carve every buffer; with base == nullptr only measures
+size_t carve(fs_ctx* c, char* base) {
+  const fs_config& f = c->cfg;
+  Carver cv{base};
+  const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn,
+            V = f.vocab;
+  const int nq = (H + 2 * Hkv) * hd;
+  const int es = c->esz;
+  c->lw.assign(c->nl, LayerW());
+  for (int l = 0; l < c->nl; l++) {
+    LayerW& w = c->lw[l];
+    w.wqkv = cv.take<char>((size_t)nq * d * es);
+    if (f.qkv_bias) w.bqkv = cv.take<char>((size_t)nq * es);
+    w.wo = cv.take<char>((size_t)d * H * hd * es);
+    w.wgu = cv.take<char>((size_t)2 * ffn * d * es);
+    w.wd = cv.take<char>((size_t)d * ffn * es);
+    w.g1 = cv.take<char>((size_t)d * es);
+    w.g2 = cv.take<char>((size_t)d * es);
+    plan_gemm(w.qkv, nq, d, c->n_sms);
+    plan_gemm(w.o, d, H * hd, c->n_sms);
+    plan_gemm(w.gu, 2 * ffn, d, c->n_sms);
+    plan_gemm(w.dn, d, ffn, c->n_sms);
+  }
+  c->emb = c->first ? cv.take<char>((size_t)V * d * es) : nullptr;
+  if (c->last) {
+    c->wh = cv.take<char>((size_t)V * d * es);
+    c->gf = cv.take<char>((size_t)d * es);
+    plan_gemm(c->head, V, d, c->n_sms);
+  }
+  c->kv_plane_elems = (size_t)Hkv * f.max_ctx * hd;
+  c->kv = cv.take<char>((size_t)c->nl * 2 * c->kv_plane_elems * es);
+  c->rope = cv.take<float2>((size_t)f.max_ctx * (hd / 2));
+  const int np = c->npad;
+  c->x = cv.take<float>((size_t)np * d);
+  c->hin = cv.take<float>((size_t)np * d);
+  // GEMM B operands: 2*np rows (bf16 hi rows, then lo rows)
+  c->y = cv.take<char>((size_t)2 * np * d * es);
+  c->q = cv.take<char>((size_t)np * H * hd * es);
+  c->att = cv.take<char>((size_t)2 * np * H * hd * es);
+  c->act = cv.take<char>((size_t)2 * np * ffn * es);
+  // fp32 path scratch: GEMM output [np][max(nq, 2ffn, V, d)]
+  size_t ymax = std::max({(size_t)nq, (size_t)2 * ffn, (size_t)V, (size_t)d});
+  c->yf = c->bf ? nullptr : cv.take<float>((size_t)np * ymax);
+  // GEMM stream-K workspace / counters (shared by the sequential GEMMs)
+  size_t wsf = 0;
+  int max_tiles = 1;
+  auto acc = [&](const GemmOp& g) {
+    wsf = std::max(wsf, (size_t)g.sh.n_tiles * g.sh.max_contrib * 128 * np);
+    max_tiles = std::max(max_tiles, g.sh.n_tiles);
+  };
+  for (auto& w : c->lw) {
+    acc(w.qkv);
+    acc(w.o);
+    acc(w.gu);
+    acc(w.dn);
+  }
+  if (c->last) acc(c->head);
+  c->gws_floats = wsf;
+  c->gws = c->bf ? cv.take<float>(wsf) : nullptr;
+  c->gcnt = cv.take<int>(max_tiles);
+  c->head_part = cv.take<Top2>((size_t)((V + 127) / 128) * np);
+  c->res = cv.take<RowResult>(FS_MAX_SEG);
+  c->out_node = cv.take<int32_t>(FS_MAX_SEG);
+  c->att_chunk_cap = (f.max_ctx + ATT_KC - 1) / ATT_KC;
+  const int G = H / Hkv;
+  c->aws_o = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * ATT_HD) : nullptr;
+  c->aws_ml = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * 2) : nullptr;
+  // tree
+  const int ML = f.max_live;
+  TreeDev& t = c->tree;
+  t.max_live = ML;
+  t.ancw = ML / 32;
+  t.max_ids = c->max_ids;
+  t.node = cv.take<int32_t>(ML);
+  t.token = cv.take<int32_t>(ML);
+  t.par = cv.take<int32_t>(ML);
+  t.own = cv.take<float>(ML);
+  t.cu = cv.take<float>(ML);
+  t.depth = cv.take<int32_t>(ML);
+  t.anc = cv.take<uint32_t>((size_t)ML * (ML / 32));
+  t.verified = cv.take<int32_t>(ML);
+  t.am = cv.take<int32_t>(ML);
+  t.margin = cv.take<float>(ML);
+  t.id2s = cv.take<int32_t>(c->max_ids);
+  t.rank = cv.take<int32_t>(ML);
+  t.retain = cv.take<uint32_t>(ML / 32);
+  c->d_sub = cv.take<SubmitIn>(1);
+  c->d_dec = cv.take<DecisionIn>(1);
+  c->d_rec = cv.take<TreeRecord>(1);
+  c->d_rows = cv.take<TickRows>(1);
+  return cv.off + 256;
+}
+
+bool setup_ctx(fs_ctx* c, const fs_config* f) {
+  c->cfg = *f;
+  c->P = f->n_stages;
+  c->rank = f->rank;
+  balance(f, c->lps);
+  c->cfg.layers_per_stage = nullptr;
+  c->L0 = 0;
+  for (int p = 0; p < c->rank; p++) c->L0 += c->lps[p];
+  c->nl = c->lps[c->rank];
+  c->L1 = c->L0 + c->nl;
+  c->first = c->rank == 0;
+  c->last = c->rank == c->P - 1;
+  c->bf = f->bf16 != 0;
+  c->esz = c->bf ? 2 : 4;
+  c->npad = npad_of(f->max_seg);
+  c->ancw = f->max_live / 32;
+  return true;
+}
+
+bool encode_map(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                uint32_t box_outer) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool build_maps(fs_ctx* c) {
+  const fs_config& f = c->cfg;
+  const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn;
+  const int nq = (H + 2 * Hkv) * hd, np = c->npad;
+  bool ok = true;
+  for (auto& w : c->lw) {
+    ok &= encode_map(&w.qkv.ta, w.wqkv, d, nq, 64, 128);
+    ok &= encode_map(&w.qkv.tb, c->y, d, 2 * np, 64, 2 * np);
+    ok &= encode_map(&w.o.ta, w.wo, H * hd, d, 64, 128);
+    ok &= encode_map(&w.o.tb, c->att, H * hd, 2 * np, 64, 2 * np);
+    ok &= encode_map(&w.gu.ta, w.wgu, d, 2 * ffn, 64, 128);
+    ok &= encode_map(&w.gu.tb, c->y, d, 2 * np, 64, 2 * np);
+    ok &= encode_map(&w.dn.ta, w.wd, ffn, d, 64, 128);
+    ok &= encode_map(&w.dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
+    w.qkv.ok = w.o.ok = w.gu.ok = w.dn.ok = ok;
+  }
+  if (c->last) {
+    ok &= encode_map(&c->head.ta, c->wh, d, f.vocab, 64, 128);
+    ok &= encode_map(&c->head.tb, c->y, d, 2 * np, 64, 2 * np);
+    c->head.ok = ok;
+  }
+  return ok;
+}
+
+// ---------------------------------------------------------------- launches
+template <int NT>
+int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<NT>::SMEM);
+    attr = true;
+  }
+  GemmShape sh = g.sh;
+  sh.ws = c->gws;
+  sh.counters = c->gcnt;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(g.grid);
+  lc.blockDim = dim3(192);
+  lc.dynamicSmemBytes = GemmCfg<NT>::SMEM;
+  lc.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, gemm_tc_kernel<NT>, g.ta, g.tb, sh, ep);
+  CK_LAUNCH(c);
+  return FS_OK;
+}
+
+int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
+  switch (c->npad) {
+    case 16: return launch_gemm_nt<16>(c, g, ep);
+    case 32: return launch_gemm_nt<32>(c, g, ep);
+    default: return launch_gemm_nt<64>(c, g, ep);
+  }
+}
+
+GemmEpi base_epi(fs_ctx* c) {
+  GemmEpi e;
+  memset(&e, 0, sizeof(e));
+  e.rows = c->d_rows;
+  e.H = c->cfg.n_heads;
+  e.Hkv = c->cfg.n_kv_heads;
+  e.max_ctx = c->cfg.max_ctx;
+  e.rope = c->rope;
+  e.ffn = c->cfg.ffn;
+  e.d = c->cfg.d_model;
+  e.vocab = c->cfg.vocab;
+  return e;
+}
+
+char* kv_plane(fs_ctx* c, int local_layer, int which) {
+  return c->kv + ((size_t)local_layer * 2 + which) * c->kv_plane_elems * c->esz;
+}
+
+// one decoder layer on the current tick rows (x in place)
+int layer_forward(fs_ctx* c, int l) {
+  const fs_config& f = c->cfg;
+  LayerW& w = c->lw[l];
+  const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn;
+  const int np = c->npad;
+  const int nq = (H + 2 * Hkv) * hd;
+  int rc;
+  if (c->bf) {
+    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)w.g1, (bf16*)c->y, d,
+                                                     (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    GemmEpi e = base_epi(c);
+    e.mode = EPI_QKV;
+    e.bias = (const bf16*)w.bqkv;
+    e.q_out = (bf16*)c->q;
+    e.k_cache = (bf16*)kv_plane(c, l, 0);
+    e.v_cache = (bf16*)kv_plane(c, l, 1);
+    if ((rc = launch_gemm(c, w.qkv, e))) return rc;
+    AttnArgs a;
+    a.q = (const bf16*)c->q;
+    a.kc = (const bf16*)kv_plane(c, l, 0);
+    a.vc = (const bf16*)kv_plane(c, l, 1);
+    a.rows = c->d_rows;
+    a.anc = c->tree.anc;
+    a.ws_o = c->aws_o;
+    a.ws_ml = c->aws_ml;
+    a.ancw = c->ancw;
+    a.max_live = f.max_live;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.max_ctx = f.max_ctx;
+    a.npad = np;
+    a.n_chunk_cap = c->att_chunk_cap;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+    const int G = H / Hkv, QR = G * np, MT = QR / 16;
+    const int KS = MT >= 4 ? 1 : 4 / MT;
+    const int n_keys = c->h_rows->n_keys;
+    const int n_chunks = (n_keys + ATT_KC - 1) / ATT_KC;
+    const size_t smem = (size_t)QR * ATT_LD * 2 + 2 * ATT_KC * ATT_LD * 2 + (size_t)np * c->ancw * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    attn_mma_kernel<<<dim3(n_chunks, Hkv), 128, smem, c->st>>>(a);
+    CK_LAUNCH(c);
+    attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, n_chunks * KS);
+    CK_LAUNCH(c);
+    e = base_epi(c);
+    e.mode = EPI_RESID;
+    e.x = c->x;
+    if ((rc = launch_gemm(c, w.o, e))) return rc;
+    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)w.g2, (bf16*)c->y, d,
+                                                     (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    e = base_epi(c);
+    e.mode = EPI_GLU;
+    e.act = (bf16*)c->act;
+    if ((rc = launch_gemm(c, w.gu, e))) return rc;
+    e = base_epi(c);
+    e.mode = EPI_RESID;
+    e.x = c->x;
+    if ((rc = launch_gemm(c, w.dn, e))) return rc;
+  } else {
+    float* yf = c->yf;
+    rmsnorm_kernel<float, float, false><<<np, 128, 0, c->st>>>(c->x, (const float*)w.g1, (float*)c->y, d,
+                                                       (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    gemm_f32_kernel<<<(nq + 127) / 128, 128, 0, c->st>>>((const float*)w.wqkv, (const float*)c->y, yf,
+                                                         nq, d, c->d_rows);
+    CK_LAUNCH(c);
+    epi_qkv_f32_kernel<<<dim3(((H + 2 * Hkv) * hd / 2 + 127) / 128, FS_MAX_SEG), 128, 0, c->st>>>(
+        yf, (const float*)w.bqkv, c->rope, (float*)c->q, (float*)kv_plane(c, l, 0),
+        (float*)kv_plane(c, l, 1), H, Hkv, hd, f.max_ctx, c->d_rows);
+    CK_LAUNCH(c);
+    const int n_keys = c->h_rows->n_keys;
+    attn_simple_kernel<float><<<dim3(H, FS_MAX_SEG), 128, (size_t)n_keys * 4, c->st>>>(
+        (const float*)c->q, (const float*)kv_plane(c, l, 0), (const float*)kv_plane(c, l, 1),
+        (float*)c->att, c->d_rows, c->tree.anc, c->ancw, f.max_live, H, Hkv, hd, f.max_ctx,
+        (float)(1.0 / std::sqrt((double)hd)));
+    CK_LAUNCH(c);
+    gemm_f32_kernel<<<(d + 127) / 128, 128, 0, c->st>>>((const float*)w.wo, (const float*)c->att, yf,
+                                                        d, H * hd, c->d_rows);
+    CK_LAUNCH(c);
+    epi_resid_f32_kernel<<<dim3((d + 127) / 128, FS_MAX_SEG), 128, 0, c->st>>>(yf, c->x, d, c->d_rows);
+    CK_LAUNCH(c);
+    rmsnorm_kernel<float, float, false><<<np, 128, 0, c->st>>>(c->x, (const float*)w.g2, (float*)c->y, d,
+                                                       (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    gemm_f32_kernel<<<(2 * ffn + 127) / 128, 128, 0, c->st>>>((const float*)w.wgu, (const float*)c->y,
+                                                              yf, 2 * ffn, d, c->d_rows);
+    CK_LAUNCH(c);
+    epi_glu_f32_kernel<<<dim3((ffn + 127) / 128, FS_MAX_SEG), 128, 0, c->st>>>(yf, (float*)c->act, ffn,
+                                                                             c->d_rows);
+    CK_LAUNCH(c);
+    gemm_f32_kernel<<<(d + 127) / 128, 128, 0, c->st>>>((const float*)w.wd, (const float*)c->act, yf,
+                                                        d, ffn, c->d_rows);
+    CK_LAUNCH(c);
+    epi_resid_f32_kernel<<<dim3((d + 127) / 128, FS_MAX_SEG), 128, 0, c->st>>>(yf, c->x, d, c->d_rows);
+    CK_LAUNCH(c);
+  }
+  return FS_OK;
+}
+
+// final RMSNorm + head + argmax/top-2 on the last stage -> c->res
+int head_forward(fs_ctx* c) {
+  const fs_config& f = c->cfg;
+  const int d = f.d_model, V = f.vocab, np = c->npad;
+  if (c->bf) {
+    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)c->gf, (bf16*)c->y, d,
+                                                     (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    GemmEpi e = base_epi(c);
+    e.mode = EPI_HEAD;
+    e.head_part = c->head_part;
+    e.logits = c->logits_buf;
+    int rc = launch_gemm(c, c->head, e);
+    if (rc) return rc;
+    argmax_final_kernel<<<FS_MAX_SEG, 32, 0, c->st>>>(c->head_part, c->head.sh.n_tiles, np, c->d_rows,
+                                                      c->res);
+    CK_LAUNCH(c);
+  } else {
+    rmsnorm_kernel<float, float, false><<<np, 128, 0, c->st>>>(c->x, (const float*)c->gf, (float*)c->y, d,
+                                                       (float)f.rms_eps, c->d_rows);
+    CK_LAUNCH(c);
+    gemm_f32_kernel<<<(V + 127) / 128, 128, 0, c->st>>>((const float*)c->wh, (const float*)c->y, c->yf,
+                                                        V, d, c->d_rows);
+    CK_LAUNCH(c);
+    argmax_rows_kernel<<<FS_MAX_SEG, 256, 0, c->st>>>(c->yf, V, c->d_rows, c->res, c->logits_buf);
+    CK_LAUNCH(c);
+  }
+  return FS_OK;
+}
+
+// this stage's forward of the rows in d_rows (h_rows mirrors it on the host)
+int stage_forward(fs_ctx* c, bool from_hin) {
+  const int d = c->cfg.d_model;
+  const int n = c->h_rows->n_rows;
+  if (c->first) {
+    if (c->bf)
+      embed_kernel<bf16><<<FS_MAX_SEG, 256, 0, c->st>>>((const bf16*)c->emb, d, c->d_rows, c->x);
+    else
+      embed_kernel<float><<<FS_MAX_SEG, 256, 0, c->st>>>((const float*)c->emb, d, c->d_rows, c->x);
+    CK_LAUNCH(c);
+  } else if (from_hin) {
+    CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
+  for (int l = 0; l < c->nl; l++) {
+    int rc = layer_forward(c, l);
+    if (rc) return rc;
+  }
+  if (c->last) return head_forward(c);
+  return FS_OK;
+}
+
+int upload_rows(fs_ctx* c) {
+  CK_CUDA(c, cudaMemcpyAsync(c->d_rows, c->h_rows, sizeof(TickRows), cudaMemcpyHostToDevice, c->st));
+  return FS_OK;
+}
+
+int sync(fs_ctx* c) {
+  CK_CUDA(c, cudaStreamSynchronize(c->st));
+  return FS_OK;
+}
+
+bool check(fs_ctx* c, int* rc) {
+  if (!c) {
+    *rc = FS_EINVAL;
+    return false;
+  }
+  if (c->poisoned) {
+    *rc = FS_EPOISONED;
+    return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+// =====================================================================  ABI
+extern "C" {
+
+size_t fs_arena_bytes(const fs_config* cfg) {
+  if (!cfg_valid(cfg, nullptr)) return 0;
+  fs_ctx tmp;
+  setup_ctx(&tmp, cfg);
+  return carve(&tmp, nullptr);
+}
+
+int fs_nccl_unique_id(uint8_t* out) {
+  if (!out) return FS_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return FS_ENCCL;
+  memcpy(out, id.internal, 128);
+  return FS_OK;
+}
+
+int fs_init(const fs_config* cfg, fs_ctx** out) {
+  if (!out) return FS_EINVAL;
+  *out = nullptr;
+  std::string why;
+  if (!cfg_valid(cfg, &why)) {
+    fprintf(stderr, "fs_init: %s\n", why.c_str());
+    return FS_EINVAL;
+  }
+  if (!cfg->arena || !cfg->stream) return FS_EINVAL;
+  if (cfg->n_stages > 1 && !cfg->nccl_id) return FS_EINVAL;
+  fs_ctx* c = new fs_ctx();
+  setup_ctx(c, cfg);
+  if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    delete c;
+    return FS_ECUDA;
+  }
+  cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  c->st = (cudaStream_t)cfg->stream;
+  const size_t need = carve(c, nullptr);
+  if (cfg->arena_bytes < need) {
+    delete c;
+    return FS_ENOMEM;
+  }
+  c->base = (char*)cfg->arena;
+  c->cap = cfg->arena_bytes;
+  carve(c, c->base);
+  if (c->bf && !build_maps(c)) {
+    delete c;
+    return FS_ECUDA;
+  }
+  if (cudaMallocHost(&c->h_sub, sizeof(SubmitIn)) || cudaMallocHost(&c->h_dec, sizeof(DecisionIn)) ||
+      cudaMallocHost(&c->h_rec, sizeof(TreeRecord)) || cudaMallocHost(&c->h_rows, sizeof(TickRows)) ||
+      cudaMallocHost(&c->h_res, sizeof(RowResult) * FS_MAX_SEG) ||
+      cudaMallocHost(&c->h_node, sizeof(int32_t) * FS_MAX_SEG)) {
+    delete c;
+    return FS_ECUDA;
+  }
+  memset(c->h_rows, 0, sizeof(TickRows));
+  // zero activations / tree; id2s = -1; counters = 0
+  cudaMemsetAsync(c->base, 0, need - 256, c->st);
+  cudaMemsetAsync(c->tree.id2s, 0xff, sizeof(int32_t) * c->max_ids, c->st);
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) {
+    delete c;
+    return FS_ECUDA;
+  }
+  if (c->P > 1) {
+    ncclUniqueId id;
+    memcpy(id.internal, cfg->nccl_id, 128);
+    if (ncclCommInitRank(&c->comm, c->P, id, c->rank) != ncclSuccess) {
+      delete c;
+      return FS_ENCCL;
+    }
+  }
+  *out = c;
+  return FS_OK;
+}
+
+int fs_load_random_weights(fs_ctx* c, uint64_t seed) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (c->weights) return fail(c, FS_ESTATE, "weights already loaded");
+  const fs_config& f = c->cfg;
+  const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn,
+            V = f.vocab, L = f.n_layers;
+  auto key = [&](uint64_t tid) {
+    // tensor key: mix(seed ^ tid * 0xD1B54A32D192ED03) (host copy of the recipe)
+    uint64_t z = seed ^ (tid * 0xD1B54A32D192ED03ull);
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  auto scale = [](double sigma, int gain) {
+    return gain ? (float)(0.1 / 16777216.0) : (float)(sigma * std::sqrt(3.0) / 16777216.0);
+  };
+  auto gen = [&](void* dst, uint64_t tid, double sigma, int gain, int64_t rows, int64_t cols,
+                 int mode, int64_t off) -> int {
+    const int64_t n = rows * cols;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    if (c->bf)
+      gen_weight_kernel<bf16><<<blocks, 256, 0, c->st>>>((bf16*)dst, key(tid), scale(sigma, gain), gain,
+                                                         rows, cols, mode, off);
+    else
+      gen_weight_kernel<float><<<blocks, 256, 0, c->st>>>((float*)dst, key(tid), scale(sigma, gain),
+                                                          gain, rows, cols, mode, off);
+    CK_LAUNCH(c);
+    return FS_OK;
+  };
+  const double s = 0.02, so = 0.02 / std::sqrt(2.0 * L);
+  for (int l = 0; l < c->nl; l++) {
+    const uint64_t gl = (uint64_t)(c->L0 + l) * 16;
+    LayerW& w = c->lw[l];
+    if ((rc = gen(w.wqkv, gl + 0, s, 0, (int64_t)H * hd, d, 0, 0))) return rc;
+    if ((rc = gen(w.wqkv, gl + 1, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)H * hd))) return rc;
+    if ((rc = gen(w.wqkv, gl + 2, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)(H + Hkv) * hd))) return rc;
+    if (f.qkv_bias) {
+      if ((rc = gen(w.bqkv, gl + 9, s, 0, 1, (int64_t)H * hd, 0, 0))) return rc;
+      char* bk = (char*)w.bqkv + (size_t)H * hd * c->esz;
+      if ((rc = gen(bk, gl + 10, s, 0, 1, (int64_t)Hkv * hd, 0, 0))) return rc;
+      char* bv = bk + (size_t)Hkv * hd * c->esz;
+      if ((rc = gen(bv, gl + 11, s, 0, 1, (int64_t)Hkv * hd, 0, 0))) return rc;
+    }
+    if ((rc = gen(w.wo, gl + 3, so, 0, d, (int64_t)H * hd, 0, 0))) return rc;
+    if ((rc = gen(w.wgu, gl + 4, s, 0, ffn, d, 1, 0))) return rc;
+    if ((rc = gen(w.wgu, gl + 5, s, 0, ffn, d, 2, 0))) return rc;
+    if ((rc = gen(w.wd, gl + 6, so, 0, d, ffn, 0, 0))) return rc;
+    if ((rc = gen(w.g1, gl + 7, 0, 1, 1, d, 0, 0))) return rc;
+    if ((rc = gen(w.g2, gl + 8, 0, 1, 1, d, 0, 0))) return rc;
+  }
+  if (c->first && (rc = gen(c->emb, 0xFFFF0, s, 0, V, d, 0, 0))) return rc;
+  if (c->last) {
+    if ((rc = gen(c->wh, 0xFFFF1, 2.0 / std::sqrt((double)d), 0, V, d, 0, 0))) return rc;
+    if ((rc = gen(c->gf, 0xFFFF2, 0, 1, 1, d, 0, 0))) return rc;
+  }
+  rope_table_kernel<<<148 * 4, 256, 0, c->st>>>(c->rope, f.max_ctx, hd / 2, f.rope_theta, hd);
+  CK_LAUNCH(c);
+  if ((rc = sync(c))) return rc;
+  c->weights = true;
+  return FS_OK;
+}
+
+int fs_set_logits_buffer(fs_ctx* c, float* dev_logits, int32_t rows_cap) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (dev_logits && rows_cap < c->cfg.max_seg) return fail(c, FS_EINVAL, "rows_cap < max_seg");
+  c->logits_buf = dev_logits;
+  c->logits_cap = rows_cap;
+  return FS_OK;
+}
+
+static void reset_round(fs_ctx* c) {
+  c->live = 0;
+  c->n_live = 0;
+  c->next_id = 0;
+  c->queue.clear();
+  for (int p = 0; p < FS_MAX_STAGES; p++) {
+    c->slot[p] = Seg();
+    c->n_cached[p] = 0;
+  }
+}
+
+// run rows (already in h_rows) through the whole pipeline without overlap:
+// stage p receives from p-1, computes, sends to p+1; the last stage leaves
+// its RowResult in c->res, which is broadcast to all ranks.
+static int run_chunk_through_pipeline(fs_ctx* c) {
+  int rc;
+  const int n = c->h_rows->n_rows;
+  const int d = c->cfg.d_model;
+  if ((rc = upload_rows(c))) return rc;
+  if (c->P > 1 && !c->first) {
+    CK_NCCL(c, ncclRecv(c->x, (size_t)n * d, ncclFloat32, c->rank - 1, c->comm, c->st));
+  }
+  if ((rc = stage_forward(c, false))) return rc;
+  if (c->P > 1 && !c->last) {
+    CK_NCCL(c, ncclSend(c->x, (size_t)n * d, ncclFloat32, c->rank + 1, c->comm, c->st));
+  }
+  if (c->P > 1) {
+    CK_NCCL(c, ncclBroadcast(c->res, c->res, sizeof(RowResult) * n / 4, ncclInt32, c->P - 1, c->comm,
+                             c->st));
+  }
+  // h_rows (pinned) is rewritten for the next chunk: the async H2D copy above
+  // must have executed first
+  return sync(c);
+}
+
+int fs_set_prefix(fs_ctx* c, const int32_t* tok, int32_t n, int32_t mode, uint64_t kv_seed,
+                  int32_t* x_new_out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!c->weights) return fail(c, FS_ESTATE, "weights not loaded");
+  if (!tok || n < 1 || (mode != FS_PREFILL && mode != FS_SYNTH_KV)) return fail(c, FS_EINVAL, "bad prefix");
+  for (int i = 0; i < n; i++)
+    if (tok[i] < 0 || tok[i] >= c->cfg.vocab) return fail(c, FS_EINVAL, "bad prefix token");
+  if (n + c->cfg.max_live > c->cfg.max_ctx) return fail(c, FS_ECAPACITY, "prefix too long");
+  reset_round(c);
+  const int M = c->cfg.max_seg;
+  int start = 0;
+  if (mode == FS_SYNTH_KV) {
+    const fs_config& f = c->cfg;
+    for (int l = 0; l < c->nl; l++)
+      for (int w = 0; w < 2; w++) {
+        uint64_t tid = 0x200000ull + (uint64_t)(c->L0 + l) * 2 + w;
+        uint64_t z = kv_seed ^ (tid * 0xD1B54A32D192ED03ull);
+        z += 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const float cc = (float)(1.0 * std::sqrt(3.0) / 16777216.0);
+        if (c->bf)
+          gen_kv_kernel<bf16><<<148 * 8, 256, 0, c->st>>>((bf16*)kv_plane(c, l, w), z, cc, f.n_kv_heads,
+                                                          f.max_ctx, f.head_dim, n - 1);
+        else
+          gen_kv_kernel<float><<<148 * 8, 256, 0, c->st>>>((float*)kv_plane(c, l, w), z, cc, f.n_kv_heads,
+                                                           f.max_ctx, f.head_dim, n - 1);
+        CK_LAUNCH(c);
+      }
+    start = n - 1;
+  }
+  while (start < n) {
+    const int m = std::min(M, n - start);
+    TickRows* r = c->h_rows;
+    r->n_rows = m;
+    r->l_glo = start;
+    r->s_begin = 0;
+    r->n_keys = start + m;
+    for (int i = 0; i < m; i++) {
+      r->token[i] = tok[start + i];
+      r->pos[i] = start + i;
+      r->slot[i] = start + i;
+      r->ctx_lim[i] = start + i + 1;
+      r->sidx[i] = -1;
+    }
+    if ((rc = run_chunk_through_pipeline(c))) return rc;
+    // keep the last row's result
+    start += m;
+    if (start >= n) {
+      CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * m, cudaMemcpyDeviceToHost, c->st));
+      if ((rc = sync(c))) return rc;
+      c->x_new = c->h_res[m - 1].am;
+    }
+  }
+  c->l_glo = n;
+  c->prefixed = true;
+  if (x_new_out) *x_new_out = c->x_new;
+  return FS_OK;
+}
+
+int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int32_t* token,
+                      const float* own, int32_t n, int32_t L_top, int32_t L_max, fs_submit_out* out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!c->prefixed) return fail(c, FS_ESTATE, "no prefix");
+  if (flags != FS_NEW_ROUND && flags != FS_APPEND) return fail(c, FS_EINVAL, "bad flags");
+  if (!parent || !token || !own || n < 1 || n > FS_MAX_LIVE || L_max < 1 || L_max > c->cfg.max_seg ||
+      L_top < 0)
+    return fail(c, FS_EINVAL, "bad submit arguments");
+  const bool nr = flags == FS_NEW_ROUND;
+  if (nr && c->live) return fail(c, FS_ESTATE, "round live");
+  if (!nr && !c->live) return fail(c, FS_ESTATE, "no live round");
+  const int base = nr ? 0 : c->next_id;
+  if (base + n > c->max_ids) return fail(c, FS_ECAPACITY, "node id space exhausted");
+  const int n_keep = (L_top > 0 && L_top < n) ? L_top : n;
+  if ((nr ? 0 : c->n_live) + n_keep > c->cfg.max_live) return fail(c, FS_ECAPACITY, "max_live");
+  if (c->l_glo + (nr ? 0 : c->n_live) + n_keep > c->cfg.max_ctx) return fail(c, FS_ECAPACITY, "max_ctx");
+  SubmitIn* s = c->h_sub;
+  s->n = n;
+  s->flags = flags;
+  s->l_top = L_top;
+  s->l_max = L_max;
+  s->base_id = base;
+  memcpy(s->parent, parent, sizeof(int32_t) * n);
+  memcpy(s->token, token, sizeof(int32_t) * n);
+  memcpy(s->own, own, sizeof(float) * n);
+  CK_CUDA(c, cudaMemcpyAsync(c->d_sub, s, sizeof(SubmitIn), cudaMemcpyHostToDevice, c->st));
+  submit_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_sub, c->d_rec, nr ? 0 : c->n_live,
+                                               c->cfg.vocab, c->x_new, nr ? 1 : 0);
+  CK_LAUNCH(c);
+  CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, acc_s), cudaMemcpyDeviceToHost, c->st));
+  if ((rc = sync(c))) return rc;
+  const TreeRecord* r = c->h_rec;
+  if (r->err) return fail(c, r->err == -4 ? FS_ECAPACITY : FS_EINVAL, "submit rejected by validation");
+  const int s_base = nr ? 0 : c->n_live;
+  if (out) {
+    out->n = r->n;
+    out->s_base = s_base;
+    memcpy(out->order, r->order, sizeof(int32_t) * r->n);
+    out->n_segs = 0;
+    out->seg_id0 = c->seg_counter;
+  }
+  // segmentation (R12): consecutive slices of <= L_max; a batch forms its own segments
+  int k = 0;
+  for (int b = 0; b < r->n; b += L_max, k++) {
+    Seg sg;
+    sg.id = c->seg_counter++;
+    sg.b = s_base + b;
+    sg.e = s_base + std::min(b + L_max, r->n);
+    c->queue.push_back(sg);
+    if (out) out->seg_begin[k] = sg.b;
+  }
+  if (out) {
+    out->n_segs = k;
+    out->seg_begin[k] = s_base + r->n;
+  }
+  c->n_live = r->n_live;
+  c->next_id = base + n;
+  c->live = 1;
+  return FS_OK;
+}
+
+int fs_verify_step(fs_ctx* c, fs_step_out* out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!c->prefixed) return fail(c, FS_ESTATE, "no prefix");
+  const int P = c->P, p = c->rank, d = c->cfg.d_model;
+  if (!c->slot[0].valid() && !c->queue.empty()) {
+    c->slot[0] = c->queue.front();
+    c->queue.pop_front();
+  }
+  const Seg cur = c->slot[p];
+  const bool has = cur.valid() && cur.n() > 0;
+  if (has) {
+    tick_setup_kernel<<<1, FS_MAX_SEG, 0, c->st>>>(c->tree, c->d_rows, cur.b, cur.n(), c->l_glo);
+    CK_LAUNCH(c);
+    // host mirror of the sizes the launch configuration needs
+    c->h_rows->n_rows = cur.n();
+    c->h_rows->n_keys = c->l_glo + cur.e;
+    if ((rc = stage_forward(c, true))) return rc;
+  }
+  // stage transport: p -> p+1 hidden rows (fp32), NCCL over NVLink
+  if (P > 1) {
+    const Seg prev = c->slot[p > 0 ? p - 1 : 0];
+    const bool recv = p > 0 && prev.valid() && prev.n() > 0;
+    const bool send = !c->last && has;
+    if (recv || send) {
+      CK_NCCL(c, ncclGroupStart());
+      if (send) CK_NCCL(c, ncclSend(c->x, (size_t)cur.n() * d, ncclFloat32, p + 1, c->comm, c->st));
+      if (recv) CK_NCCL(c, ncclRecv(c->hin, (size_t)prev.n() * d, ncclFloat32, p - 1, c->comm, c->st));
+      CK_NCCL(c, ncclGroupEnd());
+    }
+  }
+  for (int q = 0; q < P; q++)
+    if (c->slot[q].valid()) c->n_cached[q] = std::max(c->n_cached[q], c->slot[q].e);
+  const Seg outseg = c->slot[P - 1];
+  if (out) {
+    out->seg_id = outseg.valid() ? outseg.id : -1;
+    out->s_begin = outseg.b;
+    out->n_rows = outseg.valid() ? outseg.n() : 0;
+  }
+  if (outseg.valid() && outseg.n() > 0) {
+    const int n = outseg.n();
+    if (P > 1)
+      CK_NCCL(c, ncclBroadcast(c->res, c->res, (size_t)n * 2, ncclInt32, P - 1, c->comm, c->st));
+    commit_rows_kernel<<<1, FS_MAX_SEG, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->out_node);
+    CK_LAUNCH(c);
+    CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * n, cudaMemcpyDeviceToHost, c->st));
+    CK_CUDA(c, cudaMemcpyAsync(c->h_node, c->out_node, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+    if ((rc = sync(c))) return rc;
+    if (out)
+      for (int m = 0; m < n; m++) {
+        out->node[m] = c->h_node[m];
+        out->am[m] = c->h_res[m].am;
+        out->margin[m] = c->h_res[m].margin;
+      }
+  } else {
+    if ((rc = sync(c))) return rc;
+  }
+  for (int q = P - 1; q > 0; q--) c->slot[q] = c->slot[q - 1];
+  c->slot[0] = Seg();
+  return FS_OK;
+}
+
+int fs_accept(fs_ctx* c, fs_accept_out* out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!out) return fail(c, FS_EINVAL, "null out");
+  memset(out, 0, offsetof(fs_accept_out, acc_ids));
+  if (!c->live || c->n_live == 0) {
+    out->progress = 0;
+    return FS_OK;
+  }
+  accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
+  CK_LAUNCH(c);
+  CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+  if ((rc = sync(c))) return rc;
+  const TreeRecord* r = c->h_rec;
+  out->progress = r->progress;
+  if (!r->progress) return FS_OK;
+  out->n_acc = r->n_acc;
+  memcpy(out->acc_ids, r->acc_id, sizeof(int32_t) * r->n_acc);
+  memcpy(out->acc_tokens, r->acc_tok, sizeof(int32_t) * r->n_acc);
+  out->x_new = r->x_new;
+  out->n_new = r->n_new_id;
+  out->cont = r->cont;
+  out->n_flagged = r->n_flagged;
+  memcpy(out->flagged_ids, r->flagged, sizeof(int32_t) * r->n_flagged);
+  return FS_OK;
+}
+
+int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!dcs) return fail(c, FS_EINVAL, "null decision");
+  if (!c->live) return fail(c, FS_ESTATE, "no live round");
+  if (!dcs->progress || dcs->n_acc < 1 || dcs->n_acc > c->n_live) return fail(c, FS_ESTATE, "no progress");
+  DecisionIn* di = c->h_dec;
+  di->n_acc = dcs->n_acc;
+  di->n_new_id = dcs->cont ? dcs->n_new : -1;
+  di->cont = dcs->cont ? 1 : 0;
+  di->x_new = dcs->x_new;
+  memcpy(di->acc_id, dcs->acc_ids, sizeof(int32_t) * dcs->n_acc);
+  CK_CUDA(c, cudaMemcpyAsync(c->d_dec, di, sizeof(DecisionIn), cudaMemcpyHostToDevice, c->st));
+  const int n_live_old = c->n_live;
+  prune_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_dec, c->d_rec, n_live_old);
+  CK_LAUNCH(c);
+  // rank map -> host (to re-map the replicated segment schedule)
+  static thread_local std::vector<int32_t> hrank;
+  hrank.resize(c->cfg.max_live);
+  CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, order), cudaMemcpyDeviceToHost, c->st));
+  CK_CUDA(c, cudaMemcpyAsync(hrank.data(), c->tree.rank, sizeof(int32_t) * c->cfg.max_live,
+                             cudaMemcpyDeviceToHost, c->st));
+  if ((rc = sync(c))) return rc;
+  if (c->h_rec->err) return fail(c, FS_ESTATE, "inconsistent decision");
+  const int a = dcs->n_acc;
+  const bool cont = dcs->cont != 0;
+  // KV-cache pruning of this stage's layers
+  const int nc = c->n_cached[c->rank];
+  if (nc > 0) {
+    const int chunks = c->cfg.head_dim * c->esz / 16;
+    const int planes = c->nl * 2 * c->cfg.n_kv_heads;
+    if (chunks == 16)
+      kv_compact_kernel<16><<<planes, 16, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
+    else if (chunks == 4)
+      kv_compact_kernel<4><<<planes, 4, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
+    else if (chunks == 8)
+      kv_compact_kernel<8><<<planes, 8, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
+    else if (chunks == 32)
+      kv_compact_kernel<32><<<planes, 32, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
+    else
+      return fail(c, FS_EINVAL, "unsupported head_dim for compaction");
+    CK_LAUNCH(c);
+  }
+  // pruned S-index prefix: count of I_pr entries below x
+  auto pr_below = [&](int x) {
+    int k = 0;
+    for (int s = 0; s < x && s < n_live_old; s++)
+      if (hrank[s] >= 0 && hrank[s] >= a) k++;
+    return k;
+  };
+  if (cont) {
+    // in-flight rows at this stage (I_local)
+    const Seg sg = c->slot[c->rank];
+    if (c->rank > 0 && sg.valid() && sg.n() > 0) {
+      const int d4 = c->cfg.d_model / 4;
+      rows_compact_kernel<<<(d4 + 255) / 256, 256, 0, c->st>>>((float4*)c->hin, d4, c->tree.rank, sg.b, sg.n());
+      CK_LAUNCH(c);
+    }
+    for (int q = 0; q < c->P; q++) {
+      c->n_cached[q] = pr_below(c->n_cached[q]);
+      if (c->slot[q].valid()) {
+        c->slot[q].b = pr_below(c->slot[q].b);
+        c->slot[q].e = pr_below(c->slot[q].e);
+      }
+    }
+    std::deque<Seg> nq;
+    for (Seg s : c->queue) {
+      s.b = pr_below(s.b);
+      s.e = pr_below(s.e);
+      if (s.e > s.b) nq.push_back(s);
+    }
+    c->queue.swap(nq);
+    c->n_live = c->h_rec->n_pr;
+    c->l_glo += a;
+  } else {
+    c->l_glo += a;
+    c->x_new = dcs->x_new;
+    reset_round(c);
+  }
+  if ((rc = sync(c))) return rc;
+  return FS_OK;
+}
+
+int fs_query(fs_ctx* c, int32_t what, void* buf, size_t bytes, size_t* needed) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  size_t need = 0;
+  const int nl = c->n_live;
+  void* src = nullptr;
+  switch (what) {
+    case FS_Q_STATE: need = sizeof(fs_state); break;
+    case FS_Q_NODE: need = 4 * nl; src = c->tree.node; break;
+    case FS_Q_TOKEN: need = 4 * nl; src = c->tree.token; break;
+    case FS_Q_PARENT: need = 4 * nl; src = c->tree.par; break;
+    case FS_Q_POS: need = 4 * nl; src = c->tree.depth; break;
+    case FS_Q_ANC: need = (size_t)4 * nl * c->ancw; src = c->tree.anc; break;
+    case FS_Q_CU: need = 4 * nl; src = c->tree.cu; break;
+    case FS_Q_RETAIN: need = (size_t)4 * c->ancw; src = c->tree.retain; break;
+    default: return fail(c, FS_EINVAL, "bad query");
+  }
+  if (needed) *needed = need;
+  if (!buf) return FS_OK;
+  if (bytes < need) return fail(c, FS_EINVAL, "buffer too small");
+  if (what == FS_Q_STATE) {
+    fs_state* s = (fs_state*)buf;
+    memset(s, 0, sizeof(*s));
+    s->l_glo = c->l_glo;
+    s->x_new = c->x_new;
+    s->live = c->live;
+    s->n_live = c->n_live;
+    s->next_id = c->next_id;
+    s->n_stages = c->P;
+    s->rank = c->rank;
+    s->layer_begin = c->L0;
+    s->layer_end = c->L1;
+    for (int p = 0; p < c->P; p++) {
+      s->n_cached[p] = c->n_cached[p];
+      s->layers_per_stage[p] = c->lps[p];
+      s->inflight[p][0] = c->slot[p].id;
+      s->inflight[p][1] = c->slot[p].b;
+      s->inflight[p][2] = c->slot[p].e;
+    }
+    s->n_queue = (int)c->queue.size();
+    for (int i = 0; i < s->n_queue && i < FS_MAX_LIVE; i++) {
+      s->queue[i][0] = c->queue[i].id;
+      s->queue[i][1] = c->queue[i].b;
+      s->queue[i][2] = c->queue[i].e;
+    }
+    s->launches = c->launches;
+    return FS_OK;
+  }
+  if (need) {
+    CK_CUDA(c, cudaMemcpyAsync(buf, src, need, cudaMemcpyDeviceToHost, c->st));
+    if ((rc = sync(c))) return rc;
+  }
+  if (what == FS_Q_POS)
+    for (int i = 0; i < nl; i++) ((int32_t*)buf)[i] += c->l_glo;
+  return FS_OK;
+}
+
+int fs_read_kv(fs_ctx* c, int32_t layer, int32_t which, int32_t kvh, int32_t slot, float* out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  const fs_config& f = c->cfg;
+  if (!out || layer < c->L0 || layer >= c->L1 || which < 0 || which > 1 || kvh < 0 ||
+      kvh >= f.n_kv_heads || slot < 0 || slot >= f.max_ctx)
+    return fail(c, FS_EINVAL, "bad kv index");
+  const char* src = kv_plane(c, layer - c->L0, which) + ((size_t)kvh * f.max_ctx + slot) * f.head_dim * c->esz;
+  std::vector<char> tmp((size_t)f.head_dim * c->esz);
+  CK_CUDA(c, cudaMemcpyAsync(tmp.data(), src, tmp.size(), cudaMemcpyDeviceToHost, c->st));
+  if ((rc = sync(c))) return rc;
+  for (int j = 0; j < f.head_dim; j++) {
+    if (c->bf) {
+      uint32_t u = (uint32_t)((uint16_t*)tmp.data())[j] << 16;
+      memcpy(&out[j], &u, 4);
+    } else {
+      out[j] = ((float*)tmp.data())[j];
+    }
+  }
+  return FS_OK;
+}
+
+void fs_destroy(fs_ctx* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->h_sub) cudaFreeHost(c->h_sub);
+  if (c->h_dec) cudaFreeHost(c->h_dec);
+  if (c->h_rec) cudaFreeHost(c->h_rec);
+  if (c->h_rows) cudaFreeHost(c->h_rows);
+  if (c->h_res) cudaFreeHost(c->h_res);
+  if (c->h_node) cudaFreeHost(c->h_node);
+  delete c;
+}
+
+const char* fs_last_error(const fs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+const char* fs_strerror(int code) {
+  switch (code) {
+    case FS_OK: return "ok";
+    case FS_EINVAL: return "invalid argument";
+    case FS_ENOMEM: return "arena too small";
+    case FS_ESTATE: return "invalid state for this call";
+    case FS_ECAPACITY: return "capacity exceeded";
+    case FS_ECUDA: return "CUDA error (context poisoned)";
+    case FS_ENCCL: return "NCCL error (context poisoned)";
+    case FS_EPOISONED: return "context poisoned by an earlier CUDA/NCCL error";
+  }
+  return "unknown error";
+}
+
+}  // extern "C"

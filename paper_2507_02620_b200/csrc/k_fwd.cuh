@@ -1,0 +1,496 @@
+// k_fwd.cuh — decoder-layer kernels other than the tcgen05 weight GEMM:
+// embedding gather, RMSNorm, tree-masked attention (bf16 tensor-core
+// mma.sync flash-decoding with split-KV, and an fp32 CUDA-core variant for
+// the fp32 configuration), split combine, argmax/top-2, and the fp32
+// CUDA-core GEMM + epilogues used by the fp32 (no-TF32) configuration.
+#pragma once
+#include "state.cuh"
+
+namespace fs {
+
+// ---------------------------------------------------------------- embedding
+template <typename T>
+__global__ void embed_kernel(const T* __restrict__ E, int d, const TickRows* rows, float* x) {
+  const int m = blockIdx.x;
+  if (m >= rows->n_rows) return;
+  const size_t tok = (size_t)rows->token[m];
+  for (int k = threadIdx.x; k < d; k += blockDim.x) x[(size_t)m * d + k] = to_f32(E[tok * d + k]);
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// y = round(x * 1/sqrt(mean(x^2) + eps) * g)  (LLaMA RMSNorm; R18 rounding)
+// Rows >= n_rows are zero-filled (they are the padding columns of the GEMM).
+// SPLIT (bf16 path): y holds 2*npad rows, row m = bf16(v), row npad+m =
+// bf16(v - bf16(v)) (the hi/lo activation pair of the GEMM B operand).
+template <typename TW, typename TO, bool SPLIT>
+__global__ void rmsnorm_kernel(const float* __restrict__ x, const TW* __restrict__ g, TO* y,
+                               int d, float eps, const TickRows* rows) {
+  const int m = blockIdx.x;
+  TO* yr = y + (size_t)m * d;
+  TO* yl = y + (size_t)(gridDim.x + m) * d;
+  if (m >= rows->n_rows) {
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+      yr[k] = from_f32<TO>(0.f);
+      if (SPLIT) yl[k] = from_f32<TO>(0.f);
+    }
+    return;
+  }
+  const float* xr = x + (size_t)m * d;
+  float ss = 0.f;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) ss += xr[k] * xr[k];
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane_id() == 0) red[warp_id()] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    const float v = xr[k] * inv * to_f32(g[k]);
+    const TO h = from_f32<TO>(v);
+    yr[k] = h;
+    if (SPLIT) yl[k] = from_f32<TO>(v - to_f32(h));
+  }
+}
+
+// ---------------------------------------------------------------- visibility
+// Key slot k is visible to row m iff it is committed context below ctx_lim
+// (causal in prefill) or a draft slot l_glo+a with a in anc(row).
+FS_DEV bool key_visible(const TickRows* rows, int m, int k, const uint32_t* anc, int ancw,
+                        int max_live) {
+  if (k < rows->ctx_lim[m]) return true;
+  const int s = rows->sidx[m];
+  const int a = k - rows->l_glo;
+  if (s < 0 || a < 0 || a >= max_live) return false;
+  return (anc[(size_t)s * ancw + (a >> 5)] >> (a & 31)) & 1u;
+}
+
+// ---------------------------------------------------------------- fp32 attention
+// CUDA-core attention for the fp32 configuration (launch-bound sizes).
+// grid (H, MAXSEG), block 128, dyn smem n_keys_cap floats.
+template <typename T>
+__global__ void attn_simple_kernel(const T* __restrict__ q, const T* __restrict__ kc,
+                                   const T* __restrict__ vc, T* o, const TickRows* rows,
+                                   const uint32_t* anc, int ancw, int max_live, int H, int Hkv,
+                                   int hd, int max_ctx, float scale) {
+  extern __shared__ float sc[];
+  const int h = blockIdx.x, m = blockIdx.y;
+  if (m >= rows->n_rows) return;
+  const int kvh = h / (H / Hkv);
+  const int nk = rows->n_keys;
+  const T* qr = q + ((size_t)m * H + h) * hd;
+  const T* kb = kc + (size_t)kvh * max_ctx * hd;
+  const T* vb = vc + (size_t)kvh * max_ctx * hd;
+  __shared__ float red[32];
+  float mx = -INFINITY;
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    float s = -INFINITY;
+    if (key_visible(rows, m, k, anc, ancw, max_live)) {
+      float dot = 0.f;
+      for (int j = 0; j < hd; j++) dot += to_f32(qr[j]) * to_f32(kb[(size_t)k * hd + j]);
+      s = dot * scale;
+    }
+    sc[k] = s;
+    mx = fmaxf(mx, s);
+  }
+  for (int of = 16; of > 0; of >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, of));
+  if (lane_id() == 0) red[warp_id()] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < (int)blockDim.x / 32; w++) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float den = 0.f;
+  for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+    float p = (sc[k] == -INFINITY) ? 0.f : expf(sc[k] - mx);
+    sc[k] = p;
+    den += p;
+  }
+  for (int of = 16; of > 0; of >>= 1) den += __shfl_xor_sync(0xffffffffu, den, of);
+  if (lane_id() == 0) red[warp_id()] = den;
+  __syncthreads();
+  den = 0.f;
+  for (int w = 0; w < (int)blockDim.x / 32; w++) den += red[w];
+  for (int j = threadIdx.x; j < hd; j += blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < nk; k++)
+      if (sc[k] != 0.f) acc += sc[k] * to_f32(vb[(size_t)k * hd + j]);
+    o[((size_t)m * H + h) * hd + j] = from_f32<T>(acc / den);
+  }
+}
+
+// ---------------------------------------------------------------- bf16 attention
+// Split-KV flash-decoding on tensor cores (mma.sync m16n8k16 bf16 -> fp32).
+// CTA = (key chunk of ATT_KC slots, kv head).  Query rows of the CTA are the
+// G = H/Hkv heads sharing the kv head times the padded segment rows (GQA
+// packing into M).  Each CTA writes an unnormalised partial (O, m, l) per row;
+// attn_combine_kernel merges the chunks.
+constexpr int ATT_KC = 128;     // keys per CTA
+constexpr int ATT_HD = 128;     // head dim (all bf16 configs)
+constexpr int ATT_LD = ATT_HD + 8;  // padded smem row (bf16 elements): conflict-free ldmatrix
+
+FS_DEV void ldsm_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(smem_u32(p)));
+}
+FS_DEV void ldsm_x2(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
+FS_DEV void ldsm_x2_t(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
+FS_DEV void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                           uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+FS_DEV uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+FS_DEV void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+FS_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct AttnArgs {
+  const bf16* q;        // [npad][H*128]
+  const bf16* kc;       // layer K cache [Hkv][max_ctx][128]
+  const bf16* vc;
+  const TickRows* rows;
+  const uint32_t* anc;
+  float* ws_o;          // [n_chunk_cap][Hkv][QR][128]
+  float* ws_ml;         // [n_chunk_cap][Hkv][QR][2]
+  int ancw, max_live, H, Hkv, max_ctx, npad, n_chunk_cap;
+  float scale_log2;     // log2(e) / sqrt(hd)
+};
+
+// block 128 threads (4 warps); dyn smem: Q [QR][LD] + K,V [KC][LD] + anc rows
+__global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
+  extern __shared__ __align__(16) uint8_t att_smem[];
+  const int chunk = blockIdx.x, kvh = blockIdx.y;
+  const TickRows* rows = a.rows;
+  const int n_rows = rows->n_rows;
+  const int nk = rows->n_keys;
+  const int k0 = chunk * ATT_KC;
+  const int G = a.H / a.Hkv;
+  const int QR = G * a.npad;           // query rows (multiple of 16)
+  const int MT = QR / 16;              // m16 tiles
+  bf16* sQ = reinterpret_cast<bf16*>(att_smem);
+  bf16* sK = sQ + (size_t)QR * ATT_LD;
+  bf16* sV = sK + ATT_KC * ATT_LD;
+  uint32_t* sAnc = reinterpret_cast<uint32_t*>(sV + ATT_KC * ATT_LD);  // [npad][ancw]
+  if (k0 >= nk || n_rows == 0) return;
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  // ---- stage Q (GQA-packed), K, V chunk, ancestor rows
+  for (int idx = tid; idx < QR * (ATT_HD / 8); idx += 128) {
+    const int r = idx / (ATT_HD / 8), c = idx % (ATT_HD / 8);
+    const int g = r / a.npad, m = r % a.npad;
+    const bf16* src = a.q + ((size_t)m * a.H + kvh * G + g) * ATT_HD + c * 8;
+    cp_async16(sQ + (size_t)r * ATT_LD + c * 8, src);
+  }
+  const bf16* kbase = a.kc + ((size_t)kvh * a.max_ctx) * ATT_HD;
+  const bf16* vbase = a.vc + ((size_t)kvh * a.max_ctx) * ATT_HD;
+  for (int idx = tid; idx < ATT_KC * (ATT_HD / 8); idx += 128) {
+    const int r = idx / (ATT_HD / 8), c = idx % (ATT_HD / 8);
+    const int slot = min(k0 + r, a.max_ctx - 1);
+    cp_async16(sK + (size_t)r * ATT_LD + c * 8, kbase + (size_t)slot * ATT_HD + c * 8);
+    cp_async16(sV + (size_t)r * ATT_LD + c * 8, vbase + (size_t)slot * ATT_HD + c * 8);
+  }
+  for (int idx = tid; idx < a.npad * a.ancw; idx += 128) {
+    const int m = idx / a.ancw, w = idx % a.ancw;
+    const int s = (m < n_rows) ? rows->sidx[m] : -1;
+    sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- work split: m-tiles x key splits over the 4 warps
+  const int KS = (MT >= 4) ? 1 : 4 / MT;            // key splits per m-tile
+  const int keys_per = ATT_KC / KS;                 // 32, 64 or 128
+  const int g_row = lane >> 2, t4 = lane & 3;
+  for (int mt = (MT >= 4 ? warp : warp % MT); mt < MT; mt += (MT >= 4 ? 4 : MT)) {
+    const int ks = (MT >= 4) ? 0 : warp / MT;
+    const int kbeg = ks * keys_per;
+    float oacc[16][4];
+#pragma unroll
+    for (int j = 0; j < 16; j++) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+    float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+    // query rows of this thread (two rows: g_row, g_row+8)
+    int qm[2], ctx[2], sl[2];
+    for (int h2 = 0; h2 < 2; h2++) {
+      const int r = mt * 16 + g_row + 8 * h2;
+      qm[h2] = r % a.npad;
+      ctx[h2] = (qm[h2] < n_rows) ? rows->ctx_lim[qm[h2]] : 0;
+      sl[h2] = (qm[h2] < n_rows) ? rows->sidx[qm[h2]] : -1;
+    }
+    for (int kb = kbeg; kb < kbeg + keys_per; kb += 32) {
+      if (k0 + kb >= nk) break;
+      float sacc[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < ATT_HD / 16; kk++) {
+        uint32_t a0, a1, a2, a3;
+        const bf16* qa = sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8;
+        ldsm_x4(a0, a1, a2, a3, qa);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint32_t b0, b1;
+          const bf16* kp = sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8;
+          ldsm_x2(b0, b1, kp);
+          mma_bf16_16816(sacc[j], a0, a1, a2, a3, b0, b1);
+        }
+      }
+      // mask + scale (log2 domain), online softmax
+      float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int h2 = e >> 1;
+          const int key = k0 + kb + j * 8 + t4 * 2 + (e & 1);
+          bool vis = key < nk && qm[h2] < n_rows;
+          if (vis && key >= ctx[h2]) {
+            const int aa = key - rows->l_glo;
+            vis = sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
+                  ((sAnc[qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+          }
+          const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
+          sacc[j][e] = v;
+          mnew[h2] = fmaxf(mnew[h2], v);
+        }
+#pragma unroll
+      for (int h2 = 0; h2 < 2; h2++) {
+        mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 1));
+        mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 2));
+      }
+      float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+      for (int h2 = 0; h2 < 2; h2++) {
+        corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : exp2f(mrow[h2] - mnew[h2]);
+        mrow[h2] = mnew[h2];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int h2 = e >> 1;
+          const float p = (sacc[j][e] == -INFINITY) ? 0.f : exp2f(sacc[j][e] - mrow[h2]);
+          sacc[j][e] = p;
+          rs[h2] += p;
+        }
+#pragma unroll
+      for (int h2 = 0; h2 < 2; h2++) lrow[h2] = lrow[h2] * corr[h2] + rs[h2];
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        oacc[j][0] *= corr[0];
+        oacc[j][1] *= corr[0];
+        oacc[j][2] *= corr[1];
+        oacc[j][3] *= corr[1];
+      }
+      // O += P V  (P from registers as the A operand, V via ldmatrix.trans).
+      // P is split into bf16 hi + lo parts (two MMAs) so the probabilities keep
+      // ~16 mantissa bits: rounding P to one bf16 would perturb the bf16-stored
+      // attention output by a fraction of an ulp and flip its rounding often
+      // (precision contract R18: fp32 softmax and accumulation).
+#pragma unroll
+      for (int kk = 0; kk < 2; kk++) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int f = 0; f < 4; f++) {
+          const int jt = 2 * kk + (f >> 1), e0 = (f & 1) * 2;
+          const float x0 = sacc[jt][e0], x1 = sacc[jt][e0 + 1];
+          const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+          ph[f] = *reinterpret_cast<const uint32_t*>(&h);
+          pl[f] = pack_bf16(x0 - __bfloat162float(h.x), x1 - __bfloat162float(h.y));
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          uint32_t b0, b1;
+          const bf16* vp = sV + (size_t)(kb + kk * 16 + (lane & 15)) * ATT_LD + j * 8;
+          ldsm_x2_t(b0, b1, vp);
+          mma_bf16_16816(oacc[j], ph[0], ph[1], ph[2], ph[3], b0, b1);
+          mma_bf16_16816(oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
+        }
+      }
+    }
+    // row sums across the quad
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) {
+      lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 1);
+      lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 2);
+    }
+    // write the partial of (chunk, key split): slot = chunk * KS + ks
+    const int part = chunk * KS + ks;
+    for (int h2 = 0; h2 < 2; h2++) {
+      const int r = mt * 16 + g_row + 8 * h2;
+      float* wo = a.ws_o + (((size_t)part * a.Hkv + kvh) * QR + r) * ATT_HD;
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        *reinterpret_cast<float2*>(wo + j * 8 + t4 * 2) =
+            make_float2(oacc[j][2 * h2], oacc[j][2 * h2 + 1]);
+      }
+      if (t4 == 0) {
+        float* wm = a.ws_ml + (((size_t)part * a.Hkv + kvh) * QR + r) * 2;
+        wm[0] = mrow[h2];
+        wm[1] = lrow[h2];
+      }
+    }
+  }
+}
+
+// merge the split partials: o = sum_c O_c 2^(m_c - M) / sum_c l_c 2^(m_c - M)
+// grid (npad, H), block 128 (one thread per head-dim element)
+__global__ void attn_combine_kernel(AttnArgs a, bf16* out, int n_parts) {
+  const int m = blockIdx.x, h = blockIdx.y;
+  if (m >= a.rows->n_rows) return;
+  const int G = a.H / a.Hkv;
+  const int kvh = h / G, g = h % G;
+  const int QR = G * a.npad;
+  const int r = g * a.npad + m;
+  float M = -INFINITY;
+  for (int c = 0; c < n_parts; c++)
+    M = fmaxf(M, a.ws_ml[(((size_t)c * a.Hkv + kvh) * QR + r) * 2]);
+  float L = 0.f, acc = 0.f;
+  const int j = threadIdx.x;
+  for (int c = 0; c < n_parts; c++) {
+    const float* ml = a.ws_ml + (((size_t)c * a.Hkv + kvh) * QR + r) * 2;
+    if (ml[0] == -INFINITY) continue;
+    const float w = exp2f(ml[0] - M);
+    L += ml[1] * w;
+    acc += a.ws_o[(((size_t)c * a.Hkv + kvh) * QR + r) * ATT_HD + j] * w;
+  }
+  const float o = acc / L;
+  const bf16 hi = __float2bfloat16_rn(o);
+  out[((size_t)m * a.H + h) * ATT_HD + j] = hi;  // hi/lo activation pair
+  out[((size_t)(a.npad + m) * a.H + h) * ATT_HD + j] = __float2bfloat16_rn(o - __bfloat162float(hi));
+}
+
+// ---------------------------------------------------------------- argmax
+// Final argmax / top-2 over the per-tile partials of the head GEMM.
+__global__ void argmax_final_kernel(const Top2* part, int n_tiles, int nt_cols,
+                                    const TickRows* rows, RowResult* res) {
+  const int m = blockIdx.x;
+  if (m >= rows->n_rows) return;
+  Top2 t;
+  t.v1 = -INFINITY;
+  t.i1 = 0x7fffffff;
+  t.v2 = -INFINITY;
+  for (int i = threadIdx.x; i < n_tiles; i += 32) t = top2_merge(t, part[(size_t)i * nt_cols + m]);
+  t = top2_warp(t);
+  if (threadIdx.x == 0) {
+    res[m].am = t.i1;
+    res[m].margin = t.v1 - t.v2;
+  }
+}
+
+// ---------------------------------------------------------------- fp32 GEMM path
+// Y[m][n] = sum_k W[n][k] X[m][k]   (CUDA cores, fp32, no TF32) — fp32 config only
+__global__ void gemm_f32_kernel(const float* __restrict__ W, const float* __restrict__ X,
+                                float* Y, int N, int K, const TickRows* rows) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int nr = rows->n_rows;
+  for (int m = 0; m < nr; m++) {
+    float acc = 0.f;
+    for (int k = 0; k < K; k++) acc += W[(size_t)n * K + k] * X[(size_t)m * K + k];
+    Y[(size_t)m * N + n] = acc;
+  }
+}
+
+// bias + rotate-half RoPE + store q / K cache / V cache (fp32 config)
+__global__ void epi_qkv_f32_kernel(const float* Y, const float* bias, const float2* rope,
+                                   float* q_out, float* kc, float* vc, int H, int Hkv, int hd,
+                                   int max_ctx, const TickRows* rows) {
+  const int m = blockIdx.y;
+  if (m >= rows->n_rows) return;
+  const int half = hd / 2;
+  const int nheads = H + 2 * Hkv;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nheads * half) return;
+  const int hh = idx / half, i = idx % half;
+  const int N = nheads * hd;
+  float a = Y[(size_t)m * N + hh * hd + i];
+  float b = Y[(size_t)m * N + hh * hd + i + half];
+  if (bias) {
+    a += bias[hh * hd + i];
+    b += bias[hh * hd + i + half];
+  }
+  float oa = a, ob = b;
+  if (hh < H + Hkv) {
+    const float2 cs = rope[(size_t)rows->pos[m] * half + i];
+    oa = a * cs.x - b * cs.y;
+    ob = b * cs.x + a * cs.y;
+  }
+  if (hh < H) {
+    q_out[((size_t)m * H + hh) * hd + i] = oa;
+    q_out[((size_t)m * H + hh) * hd + i + half] = ob;
+  } else {
+    float* dst = (hh < H + Hkv) ? kc + ((size_t)(hh - H) * max_ctx + rows->slot[m]) * hd
+                                : vc + ((size_t)(hh - H - Hkv) * max_ctx + rows->slot[m]) * hd;
+    dst[i] = oa;
+    dst[i + half] = ob;
+  }
+}
+
+// silu(gate) * up with the 64-row interleaved gate/up layout (fp32 config)
+__global__ void epi_glu_f32_kernel(const float* Y, float* act, int ffn, const TickRows* rows) {
+  const int m = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows->n_rows || j >= ffn) return;
+  const size_t base = (size_t)m * 2 * ffn + (size_t)(j / 64) * 128 + (j % 64);
+  const float g = Y[base], u = Y[base + 64];
+  act[(size_t)m * ffn + j] = g / (1.0f + expf(-g)) * u;
+}
+
+__global__ void epi_resid_f32_kernel(const float* Y, float* x, int N, const TickRows* rows) {
+  const int m = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= rows->n_rows || n >= N) return;
+  x[(size_t)m * N + n] += Y[(size_t)m * N + n];
+}
+
+// argmax/top-2 of fp32 logits rows; optional copy to the parity buffer
+__global__ void argmax_rows_kernel(const float* Y, int V, const TickRows* rows, RowResult* res,
+                                   float* logits_out) {
+  const int m = blockIdx.x;
+  if (m >= rows->n_rows) return;
+  Top2 t;
+  t.v1 = -INFINITY;
+  t.i1 = 0x7fffffff;
+  t.v2 = -INFINITY;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float y = Y[(size_t)m * V + v];
+    if (logits_out) logits_out[(size_t)m * V + v] = y;
+    Top2 u;
+    u.v1 = y;
+    u.i1 = v;
+    u.v2 = -INFINITY;
+    t = top2_merge(t, u);
+  }
+  t = top2_warp(t);
+  __shared__ Top2 sm[32];
+  if (lane_id() == 0) sm[warp_id()] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Top2 r = sm[0];
+    for (int w = 1; w < (int)blockDim.x / 32; w++) r = top2_merge(r, sm[w]);
+    res[m].am = r.i1;
+    res[m].margin = r.v1 - r.v2;
+  }
+}
+
+}  // namespace fs

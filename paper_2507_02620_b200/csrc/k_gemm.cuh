@@ -1,0 +1,340 @@
+// k_gemm.cuh — small-M weight-streaming GEMM on 5th-gen tensor cores.
+//
+//   Y[m][n] = sum_k W[n][k] * X[m][k]     W: [N_out, K] bf16 (HF [out,in]),
+//                                          X: [NT, K] bf16 activations
+// Swap-AB: the weight tile is the UMMA A operand (M = 128 output rows), the
+// NT (16/32/64) segment rows are the UMMA N dimension, the accumulator lives in
+// TMEM (128 lanes x NT fp32 columns).  A and B tiles (64 K-elements, 128-byte
+// swizzle) are staged by TMA into a STAGES-deep mbarrier ring; one elected
+// thread issues tcgen05.mma; 4 epilogue warps read TMEM with tcgen05.ld.
+//
+// Work split: stream-K over units = (128-row tile, 64-wide k block).  Grid =
+// min(#SMs, units); CTA c owns units [c*U/G, (c+1)*U/G), so every SM streams
+// the same number of weight bytes (HBM-bound: M=16..64 is far below the ridge).
+// A tile split across CTAs is reduced deterministically: every contributor
+// writes an fp32 partial, the last to arrive (atomic counter) sums them in
+// contributor order and runs the fused epilogue:
+//   EPI_QKV   + bias, rotate-half RoPE at the row's position, bf16 -> Q / K
+//             cache / V cache at the row's slot (K/V appended before attention)
+//   EPI_GLU   silu(gate) * up with 64-row interleaved gate/up weights -> bf16
+//   EPI_RESID residual += (fp32), one writer per element
+//   EPI_HEAD  logits (optional fp32 copy) + per-tile top-2 for the argmax
+//   EPI_STORE plain fp32 store (unit tests)
+#pragma once
+#include "state.cuh"
+
+namespace fs {
+
+enum { EPI_QKV = 0, EPI_GLU = 1, EPI_RESID = 2, EPI_HEAD = 3, EPI_STORE = 4 };
+
+struct GemmShape {
+  int n_out, K, kb_total, n_tiles, units, max_contrib;
+  float* ws;       // [n_tiles][max_contrib][128][NT] fp32 partials
+  int* counters;   // [n_tiles], zero between launches
+};
+
+struct GemmEpi {
+  int mode;
+  const TickRows* rows;
+  // QKV
+  const bf16* bias;
+  const float2* rope;  // [max_ctx][64] (cos, sin)
+  bf16* q_out;         // [npad][H*128]
+  bf16* k_cache;       // this layer: [Hkv][max_ctx][128]
+  bf16* v_cache;
+  int H, Hkv, max_ctx;
+  // GLU
+  bf16* act;
+  int ffn;
+  // RESID
+  float* x;
+  int d;
+  // HEAD
+  Top2* head_part;     // [n_tiles][NT]
+  float* logits;       // optional [rows][vocab]
+  int vocab;
+  // STORE
+  float* out;
+  int ldo;
+};
+
+// The activation operand carries each fp32 value as two bf16 rows (hi, lo:
+// rows [0,NT) and [NT,2NT) of the B tile), so UMMA N = 2*NT and the epilogue
+// adds the two accumulator halves: the GEMM sees ~16-bit-mantissa activations
+// at no HBM cost (the weights dominate the bytes).
+template <int NT>
+struct GemmCfg {
+  static constexpr int BN = 2 * NT;                      // UMMA N
+  static constexpr int A_BYTES = 128 * 64 * 2;           // 16 KB weight tile
+  static constexpr int B_BYTES = BN * 64 * 2;            // activation tile (hi|lo)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = NT <= 16 ? 9 : (NT <= 32 ? 8 : 5);
+  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int XCH_BYTES = 128 * (NT + 1) * 4;
+  static constexpr int TOP_BYTES = 4 * NT * (int)sizeof(Top2);
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + XCH_BYTES + TOP_BYTES;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+FS_DEV int cta_of_unit(int u, int units, int G) {
+  // largest c with floor(c*U/G) <= u
+  return (int)(((long long)(u + 1) * G + units - 1) / units) - 1;
+}
+
+template <int NT>
+FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
+                          float* xch, Top2* stop) {
+  const TickRows* rows = ep.rows;
+  const int n_rows = rows->n_rows;
+  const int ng = t * 128 + row;
+  const int lane = lane_id(), q = warp_id() & 3;
+  if (ep.mode == EPI_QKV) {
+    const int H = ep.H, Hkv = ep.Hkv;
+    if (ep.bias) {
+      const float b = to_f32(ep.bias[ng]);
+#pragma unroll
+      for (int m = 0; m < NT; m++) v[m] += b;
+    }
+    const int hh = t;  // one head (128 rows) per tile
+    if (hh < H + Hkv) {  // rotate-half RoPE on q and k heads
+#pragma unroll
+      for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
+      named_bar_sync(1, 128);
+      const int i = row & 63;
+#pragma unroll
+      for (int m = 0; m < NT; m++) {
+        const float pv = xch[(row ^ 64) * (NT + 1) + m];
+        if (m < n_rows) {
+          const float2 cs = ep.rope[(size_t)rows->pos[m] * 64 + i];
+          v[m] = (row < 64) ? (v[m] * cs.x - pv * cs.y) : (v[m] * cs.x + pv * cs.y);
+        }
+      }
+      named_bar_sync(1, 128);
+    }
+    for (int m = 0; m < n_rows && m < NT; m++) {
+      const bf16 o = __float2bfloat16_rn(v[m]);
+      if (hh < H) {
+        ep.q_out[((size_t)m * H + hh) * 128 + row] = o;
+      } else if (hh < H + Hkv) {
+        ep.k_cache[((size_t)(hh - H) * ep.max_ctx + rows->slot[m]) * 128 + row] = o;
+      } else {
+        ep.v_cache[((size_t)(hh - H - Hkv) * ep.max_ctx + rows->slot[m]) * 128 + row] = o;
+      }
+    }
+  } else if (ep.mode == EPI_GLU) {
+#pragma unroll
+    for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
+    named_bar_sync(1, 128);
+    if (row < 64) {
+      for (int m = 0; m < n_rows && m < NT; m++) {
+        const float g = v[m], u = xch[(row + 64) * (NT + 1) + m];
+        const float a = g / (1.0f + expf(-g)) * u;
+        const bf16 hi = __float2bfloat16_rn(a);
+        ep.act[(size_t)m * ep.ffn + t * 64 + row] = hi;
+        ep.act[(size_t)(NT + m) * ep.ffn + t * 64 + row] = __float2bfloat16_rn(a - __bfloat162float(hi));
+      }
+    }
+    named_bar_sync(1, 128);
+  } else if (ep.mode == EPI_RESID) {
+    if (ng < sh.n_out)
+      for (int m = 0; m < n_rows && m < NT; m++) ep.x[(size_t)m * ep.d + ng] += v[m];
+  } else if (ep.mode == EPI_HEAD) {
+    const bool valid = ng < ep.vocab;
+    if (ep.logits && valid)
+      for (int m = 0; m < n_rows && m < NT; m++) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
+#pragma unroll
+    for (int m = 0; m < NT; m++) {
+      Top2 tt;
+      tt.v1 = valid ? v[m] : -INFINITY;
+      tt.i1 = valid ? ng : 0x7fffffff;
+      tt.v2 = -INFINITY;
+      tt = top2_warp(tt);
+      if (lane == 0) stop[q * NT + m] = tt;
+    }
+    named_bar_sync(1, 128);
+    if (row < NT) {
+      Top2 r = stop[row];
+      for (int w = 1; w < 4; w++) r = top2_merge(r, stop[w * NT + row]);
+      ep.head_part[(size_t)t * NT + row] = r;
+    }
+    named_bar_sync(1, 128);
+  } else {  // EPI_STORE
+    if (ng < sh.n_out)
+      for (int m = 0; m < n_rows && m < NT; m++) ep.out[(size_t)m * ep.ldo + ng] = v[m];
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   GemmShape sh, GemmEpi ep) {
+  using C = GemmCfg<NT>;
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int* s_flag = reinterpret_cast<int*>(tmem_holder + 1);
+  float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
+  Top2* stop = reinterpret_cast<Top2*>(reinterpret_cast<uint8_t*>(xch) + C::XCH_BYTES);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int G = gridDim.x, c = blockIdx.x;
+  const int U = sh.units, KB = sh.kb_total;
+  const int u0 = (int)((long long)c * U / G), u1 = (int)((long long)(c + 1) * U / G);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: weights never depend on the previous
+    // kernel, so they stream before the grid dependency resolves (PDL).
+    if (lane == 0) {
+      const uint64_t polA = l2_evict_first_policy();
+      const uint64_t polB = l2_evict_last_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      const int pre = min(u1 - u0, C::STAGES);
+      for (int i = 0; i < pre; i++) {
+        const int u = u0 + i;
+        mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (u % KB) * 64, (u / KB) * 128, polA);
+      }
+      pdl_wait();  // activations (B) are produced by the previous kernel
+      for (int i = 0; i < pre; i++) {
+        const int u = u0 + i;
+        tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (u % KB) * 64, 0, polB);
+      }
+      stage = pre % C::STAGES;
+      phase = (pre == C::STAGES) ? 1 : 0;
+      for (int u = u0 + pre; u < u1; u++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], (u % KB) * 64, (u / KB) * 128, polA);
+        tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], (u % KB) * 64, 0, polB);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(128, C::BN);
+      int stage = 0, seg = 0;
+      uint32_t phase = 0;
+      int u = u0;
+      while (u < u1) {
+        const int t = u / KB;
+        const int seg_start = u, seg_end = min(u1, (t + 1) * KB);
+        if (seg > 0) mbar_wait(acc_empty, (seg - 1) & 1);
+        tc_fence_after();
+        for (; u < seg_end; u++) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; k++)
+            umma_bf16(tmem, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
+                      (u > seg_start || k > 0) ? 1u : 0u);
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(acc_full);
+        seg++;
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int seg = 0, u = u0;
+    while (u < u1) {
+      const int t = u / KB;
+      const int seg_start = u, seg_end = min(u1, (t + 1) * KB);
+      mbar_wait(acc_full, seg & 1);
+      tc_fence_after();
+      float v[NT];
+      const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+      for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
+#pragma unroll
+      for (int j = 0; j < NT; j += 16) {  // + lo half of the activation pair
+        float w[16];
+        tmem_ld16(tl + NT + j, w);
+#pragma unroll
+        for (int i = 0; i < 16; i++) v[j + i] += w[i];
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty);
+      const bool whole = (seg_start == t * KB) && (seg_end == (t + 1) * KB);
+      bool run_epi = whole;
+      if (!whole) {
+        const int cf = cta_of_unit(t * KB, U, G);
+        const int cl = cta_of_unit((t + 1) * KB - 1, U, G);
+        const int j = c - cf, nc = cl - cf + 1;
+        float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
+#pragma unroll
+        for (int m = 0; m < NT; m += 4)
+          *reinterpret_cast<float4*>(wp + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) *s_flag = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+        named_bar_sync(1, 128);
+        run_epi = *s_flag;
+        if (run_epi) {
+          __threadfence();
+#pragma unroll
+          for (int m = 0; m < NT; m++) v[m] = 0.f;
+          for (int jj = 0; jj < nc; jj++) {
+            const float* rp = sh.ws + (((size_t)t * sh.max_contrib + jj) * 128 + row) * NT;
+#pragma unroll
+            for (int m = 0; m < NT; m += 4) {
+              const float4 p = __ldcg(reinterpret_cast<const float4*>(rp + m));
+              v[m] += p.x;
+              v[m + 1] += p.y;
+              v[m + 2] += p.z;
+              v[m + 3] += p.w;
+            }
+          }
+          if (warp == 2 && lane == 0) sh.counters[t] = 0;
+        }
+        named_bar_sync(1, 128);
+      }
+      if (run_epi) gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop);
+      u = seg_end;
+      seg++;
+    }
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace fs

@@ -1,0 +1,85 @@
+"""The C-ABI library builds, loads and exports every symbol include/flowspec.h
+declares; host-only entry points behave.  No GPU compute here."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2507_02620_b200 import build as B
+from synth.configs import SHAPES
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def fsmod():
+    B.build()
+    from paper_2507_02620_b200 import flowspec
+    return flowspec
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "flowspec.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(fs_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_every_declared_symbol_is_exported(fsmod):
+    lib = fsmod.lib()
+    names = declared_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(fsmod.EXPORTS) == names
+
+
+def test_struct_sizes_match_header(fsmod):
+    # offsets the binding relies on: compile a probe against the header
+    import subprocess, tempfile
+    probe = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "flowspec.h"
+int main(){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(fs_config), sizeof(fs_submit_out),
+ sizeof(fs_step_out), sizeof(fs_accept_out), sizeof(fs_state), offsetof(fs_state, launches));return 0;}
+"""
+    with tempfile.TemporaryDirectory() as d:
+        cpath = os.path.join(d, "p.c")
+        open(cpath, "w").write(probe)
+        exe = os.path.join(d, "p")
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), cpath, "-o", exe])
+        got = [int(x) for x in subprocess.check_output([exe]).split()]
+    want = [C.sizeof(fsmod.fs_config), C.sizeof(fsmod.fs_submit_out), C.sizeof(fsmod.fs_step_out),
+            C.sizeof(fsmod.fs_accept_out), C.sizeof(fsmod.fs_state), fsmod.fs_state.launches.offset]
+    assert got == want
+
+
+def test_host_only_entry_points(fsmod):
+    lib = fsmod.lib()
+    assert lib.fs_strerror(0) == b"ok"
+    assert b"poisoned" in lib.fs_strerror(-7)
+    cfg = fsmod.make_config(SHAPES["7b"], max_ctx=2048, max_seg=16)
+    n = lib.fs_arena_bytes(C.byref(cfg))
+    # 7B bf16 weights (13.5 GB) + KV (32 layers x 2 x 32 heads x 2048 x 128 x 2 B)
+    assert 13.4e9 < n < 16e9
+    cfg4 = fsmod.make_config(SHAPES["7b"], n_stages=4, rank=3, max_ctx=2048, max_seg=16)
+    n4 = lib.fs_arena_bytes(C.byref(cfg4))
+    assert n4 < n / 3
+    bad = fsmod.make_config(SHAPES["7b"], max_live=500)
+    assert lib.fs_arena_bytes(C.byref(bad)) == 0
+    h = C.c_void_p()
+    assert lib.fs_init(C.byref(bad), C.byref(h)) == fsmod.FS_EINVAL
+    assert lib.fs_init(C.byref(cfg), None) == fsmod.FS_EINVAL
+
+
+def test_no_oracle_in_product_path():
+    pkg = os.path.join(ROOT, "paper_2507_02620_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower().replace("oracle/", ""), f
+    so = open(os.path.join(pkg, "libflowspec.so"), "rb").read()
+    assert b"fso_" not in so
