@@ -206,6 +206,22 @@ int fs_query(fs_ctx* ctx, int32_t what, void* buf, size_t bytes, size_t* needed)
 int fs_read_kv(fs_ctx* ctx, int32_t layer, int32_t which, int32_t kv_head,
                int32_t slot, float* out);
 
+/* ---- measurement ---- */
+typedef struct fs_profile {
+  uint64_t gemm_launches;   /* tcgen05 weight-GEMM launches (bf16) / fp32 GEMMs */
+  double gemm_ms;           /* sum of their CUDA-event durations */
+  double gemm_bytes;        /* algorithmic bytes: weights + bf16 activation
+                               pair (2 x npad x K x 2) + outputs (rows x N x 4) */
+  uint64_t attn_launches;   /* tree-attention launches (split-KV kernel) */
+  double attn_ms;
+  double attn_bytes;        /* K and V rows of all visible-key chunks + Q + partials */
+} fs_profile;
+/* on != 0: record a CUDA event pair (on the library stream) around every
+ * weight-GEMM and attention launch; off by default (no events recorded). */
+int fs_set_profiling(fs_ctx* ctx, int32_t on);
+/* Synchronise, sum the recorded event pairs into *out and reset. */
+int fs_get_profile(fs_ctx* ctx, fs_profile* out);
+
 void fs_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);
 const char* fs_strerror(int code);

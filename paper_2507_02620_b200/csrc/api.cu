@@ -120,6 +120,11 @@ struct fs_ctx {
   uint64_t launches = 0;
   float* logits_buf = nullptr;
   int logits_cap = 0;
+  // profiling: event pairs around GEMM / attention launches
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, double>> ev_used;  // (kind 0 gemm / 1 attn, bytes) per pair
+  size_t ev_next = 0;
 };
 
 namespace {
@@ -392,6 +397,28 @@ bool build_maps(fs_ctx* c) {
   return ok;
 }
 
+// ---------------------------------------------------------------- profiling
+// returns the index of the event pair whose start was recorded, or -1
+int prof_begin(fs_ctx* c, int kind, double bytes) {
+  if (!c->prof) return -1;
+  if (c->ev_next + 2 > c->ev_pool.size()) {
+    for (int i = 0; i < 512; i++) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      c->ev_pool.push_back(e);
+    }
+  }
+  const int idx = (int)(c->ev_next / 2);
+  cudaEventRecord(c->ev_pool[c->ev_next], c->st);
+  c->ev_next += 2;
+  c->ev_used.push_back({kind, bytes});
+  return idx;
+}
+void prof_end(fs_ctx* c, int idx) {
+  if (idx < 0) return;
+  cudaEventRecord(c->ev_pool[2 * idx + 1], c->st);
+}
+
 // ---------------------------------------------------------------- launches
 template <int NT>
 int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
@@ -420,11 +447,17 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
 }
 
 int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
+  const double bytes = (double)g.sh.n_out * g.sh.K * 2 + 2.0 * c->npad * g.sh.K * 2 +
+                       (double)c->h_rows->n_rows * g.sh.n_out * 4;
+  const int pi = prof_begin(c, 0, bytes);
+  int rc;
   switch (c->npad) {
-    case 16: return launch_gemm_nt<16>(c, g, ep);
-    case 32: return launch_gemm_nt<32>(c, g, ep);
-    default: return launch_gemm_nt<64>(c, g, ep);
+    case 16: rc = launch_gemm_nt<16>(c, g, ep); break;
+    case 32: rc = launch_gemm_nt<32>(c, g, ep); break;
+    default: rc = launch_gemm_nt<64>(c, g, ep); break;
   }
+  prof_end(c, pi);
+  return rc;
 }
 
 GemmEpi base_epi(fs_ctx* c) {
@@ -490,7 +523,10 @@ int layer_forward(fs_ctx* c, int l) {
       cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
+    const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
+                                         (double)n_chunks * KS * Hkv * QR * (hd + 2) * 4);
     attn_mma_kernel<<<dim3(n_chunks, Hkv), 128, smem, c->st>>>(a);
+    prof_end(c, api);
     CK_LAUNCH(c);
     attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, n_chunks * KS);
     CK_LAUNCH(c);
@@ -1183,8 +1219,40 @@ int fs_read_kv(fs_ctx* c, int32_t layer, int32_t which, int32_t kvh, int32_t slo
   return FS_OK;
 }
 
+int fs_set_profiling(fs_ctx* c, int32_t on) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  c->prof = on != 0;
+  return FS_OK;
+}
+
+int fs_get_profile(fs_ctx* c, fs_profile* out) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!out) return fail(c, FS_EINVAL, "null out");
+  memset(out, 0, sizeof(*out));
+  if ((rc = sync(c))) return rc;
+  for (size_t i = 0; i < c->ev_used.size(); i++) {
+    float ms = 0.f;
+    CK_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]));
+    if (c->ev_used[i].first == 0) {
+      out->gemm_launches++;
+      out->gemm_ms += ms;
+      out->gemm_bytes += c->ev_used[i].second;
+    } else {
+      out->attn_launches++;
+      out->attn_ms += ms;
+      out->attn_bytes += c->ev_used[i].second;
+    }
+  }
+  c->ev_used.clear();
+  c->ev_next = 0;
+  return FS_OK;
+}
+
 void fs_destroy(fs_ctx* c) {
   if (!c) return;
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_sub) cudaFreeHost(c->h_sub);
   if (c->h_dec) cudaFreeHost(c->h_dec);

@@ -57,10 +57,16 @@ class fs_state(C.Structure):
                 ("inflight", (i32 * 3) * FS_MAX_STAGES), ("launches", C.c_uint64)]
 
 
-EXPORTS = ["fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
+class fs_profile(C.Structure):
+    _fields_ = [("gemm_launches", C.c_uint64), ("gemm_ms", C.c_double), ("gemm_bytes", C.c_double),
+                ("attn_launches", C.c_uint64), ("attn_ms", C.c_double), ("attn_bytes", C.c_double)]
+
+
+EXPORTS = ["fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
            "fs_last_error", "fs_strerror"]
+EXPORTS.sort()
 
 _lib = None
 
@@ -88,6 +94,8 @@ def lib():
         L.fs_prune_and_compact.argtypes = [P, C.POINTER(fs_accept_out)]
         L.fs_query.argtypes = [P, i32, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
         L.fs_read_kv.argtypes = [P, i32, i32, i32, i32, C.POINTER(C.c_float)]
+        L.fs_set_profiling.argtypes = [P, i32]
+        L.fs_get_profile.argtypes = [P, C.POINTER(fs_profile)]
         L.fs_destroy.argtypes = [P]
         L.fs_last_error.restype = C.c_char_p
         L.fs_last_error.argtypes = [P]
@@ -263,6 +271,14 @@ class Pipeline:
         buf = np.zeros(max(n, 1), dt)
         self._chk(self.L.fs_query(self.h, what, buf.ctypes.data, buf.nbytes, None), "fs_query")
         return buf[:n]
+
+    def set_profiling(self, on):
+        self._chk(self.L.fs_set_profiling(self.h, 1 if on else 0), "fs_set_profiling")
+
+    def get_profile(self):
+        p = fs_profile()
+        self._chk(self.L.fs_get_profile(self.h, C.byref(p)), "fs_get_profile")
+        return {k: getattr(p, k) for k, _ in fs_profile._fields_}
 
     def read_kv(self, layer, which, kvh, slot):
         out = np.zeros(self.shape.head_dim, np.float32)
