@@ -222,6 +222,14 @@ int fs_set_profiling(fs_ctx* ctx, int32_t on);
 /* Synchronise, sum the recorded event pairs into *out and reset. */
 int fs_get_profile(fs_ctx* ctx, fs_profile* out);
 
+/* Kernel microbenchmark on the rows of the last tick / prefill chunk:
+ * kind 0..3 = layer-0 QKV / O / gate-up / down GEMM, 4 = head GEMM (last
+ * stage), 5 = layer-0 attention, 6 = RMSNorm, 7 = whole stage forward.
+ * Launches back to back `iters` times on the library stream and returns the
+ * mean CUDA-event time per launch in *us and the algorithmic bytes per
+ * launch in *bytes.  Overwrites activations (not the KV context). */
+int fs_bench_kernel(fs_ctx* ctx, int32_t kind, int32_t iters, double* us, double* bytes);
+
 void fs_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);
 const char* fs_strerror(int code);

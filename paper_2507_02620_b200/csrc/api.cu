@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <deque>
 #include <string>
 #include <vector>
@@ -95,6 +96,14 @@ struct fs_ctx {
   RowResult* res = nullptr;
   int32_t* out_node = nullptr;
   float *aws_o = nullptr, *aws_ml = nullptr;
+  int* att_cnt = nullptr;
+  unsigned long long* att_dbg = nullptr;  // FS_ATT_DEBUG diagnostics only
+  unsigned long long* gemm_dbg = nullptr;
+  // CUDA graph of one tick's stage forward (replayed every tick)
+  cudaGraphExec_t fwd_exec = nullptr;
+  uint64_t fwd_kernels = 0;
+  float* fwd_logits = nullptr;
+  bool use_graph = true;
   int att_chunk_cap = 0;
   size_t gws_floats = 0;
   // tree
@@ -197,6 +206,7 @@ bool cfg_valid(const fs_config* c, std::string* why) {
   if (c->max_live < 32 || c->max_live > FS_MAX_LIVE || c->max_live % 32) return bad("max_live");
   if (c->max_seg < 1 || c->max_seg > FS_MAX_SEG) return bad("max_seg");
   if (c->max_ctx < c->max_live + 2) return bad("max_ctx");
+  if (!c->bf16 && c->max_ctx > 50000) return bad("fp32 path: max_ctx <= 50000 (attention scores in smem)");
   if (c->rms_eps <= 0 || c->rope_theta <= 0) return bad("eps/theta");
   return true;
 }
@@ -315,6 +325,7 @@ size_t carve(fs_ctx* c, char* base) {
   const int G = H / Hkv;
   c->aws_o = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * ATT_HD) : nullptr;
   c->aws_ml = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * 2) : nullptr;
+  c->att_cnt = cv.take<int>(Hkv);
   // tree
   const int ML = f.max_live;
   TreeDev& t = c->tree;
@@ -431,6 +442,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   GemmShape sh = g.sh;
   sh.ws = c->gws;
   sh.counters = c->gcnt;
+  sh.dbg = c->gemm_dbg;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(g.grid);
   lc.blockDim = dim3(192);
@@ -478,6 +490,85 @@ char* kv_plane(fs_ctx* c, int local_layer, int which) {
   return c->kv + ((size_t)local_layer * 2 + which) * c->kv_plane_elems * c->esz;
 }
 
+// tree-masked attention of local layer l on the current rows -> c->att (hi/lo)
+int launch_attention(fs_ctx* c, int l) {
+  const fs_config& f = c->cfg;
+  const int H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim;
+  const int np = c->npad;
+    AttnArgs a;
+    a.q = (const bf16*)c->q;
+    a.kc = (const bf16*)kv_plane(c, l, 0);
+    a.vc = (const bf16*)kv_plane(c, l, 1);
+    a.rows = c->d_rows;
+    a.anc = c->tree.anc;
+    a.ws_o = c->aws_o;
+    a.ws_ml = c->aws_ml;
+    a.ancw = c->ancw;
+    a.max_live = f.max_live;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.max_ctx = f.max_ctx;
+    a.npad = np;
+    a.n_chunk_cap = c->att_chunk_cap;
+    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+    a.dbg = c->att_dbg;
+    const int G = H / Hkv, QR = G * np, MT = QR / 16;
+    const int KS = MT >= 4 ? 1 : 4 / MT;
+    const int n_keys = c->h_rows->n_keys;
+    if (MT <= 2) {
+      // MHA path: key splits of one kv head form a cluster (DSMEM merge), PDL launch
+      AttnMhaArgs ma;
+      ma.a = a;
+      ma.out = (bf16*)c->att;
+      const int nsplit = 8;   // cluster of 8 key splits per kv head (sizes read on device)
+      const size_t smem = (size_t)QR * ATT_LD * 2 + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD * 2 +
+                          (size_t)np * c->ancw * 4;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(nsplit, Hkv);
+      lc.blockDim = dim3(128);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = c->st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      at[1].id = cudaLaunchAttributeClusterDimension;
+      at[1].val.clusterDim.x = nsplit;
+      at[1].val.clusterDim.y = 1;
+      at[1].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 2;
+      static bool mattr = false;
+      if (!mattr) {
+        cudaFuncSetAttribute(attn_mha_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(attn_mha_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        mattr = true;
+      }
+      const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 * 3);
+      if (MT == 1)
+        cudaLaunchKernelEx(&lc, attn_mha_kernel<16>, ma);
+      else
+        cudaLaunchKernelEx(&lc, attn_mha_kernel<32>, ma);
+      prof_end(c, api);
+      CK_LAUNCH(c);
+    } else {
+    const int n_chunks = (n_keys + ATT_KC - 1) / ATT_KC;
+    const size_t smem = (size_t)QR * ATT_LD * 2 + 2 * ATT_KC * ATT_LD * 2 + (size_t)np * c->ancw * 4;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
+                                         (double)n_chunks * KS * Hkv * QR * (hd + 2) * 4);
+    attn_mma_kernel<<<dim3(c->att_chunk_cap, Hkv), 128, smem, c->st>>>(a);
+    prof_end(c, api);
+    CK_LAUNCH(c);
+    attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, KS);
+    CK_LAUNCH(c);
+    }
+  return FS_OK;
+}
+
 // one decoder layer on the current tick rows (x in place)
 int layer_forward(fs_ctx* c, int l) {
   const fs_config& f = c->cfg;
@@ -497,39 +588,7 @@ int layer_forward(fs_ctx* c, int l) {
     e.k_cache = (bf16*)kv_plane(c, l, 0);
     e.v_cache = (bf16*)kv_plane(c, l, 1);
     if ((rc = launch_gemm(c, w.qkv, e))) return rc;
-    AttnArgs a;
-    a.q = (const bf16*)c->q;
-    a.kc = (const bf16*)kv_plane(c, l, 0);
-    a.vc = (const bf16*)kv_plane(c, l, 1);
-    a.rows = c->d_rows;
-    a.anc = c->tree.anc;
-    a.ws_o = c->aws_o;
-    a.ws_ml = c->aws_ml;
-    a.ancw = c->ancw;
-    a.max_live = f.max_live;
-    a.H = H;
-    a.Hkv = Hkv;
-    a.max_ctx = f.max_ctx;
-    a.npad = np;
-    a.n_chunk_cap = c->att_chunk_cap;
-    a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
-    const int G = H / Hkv, QR = G * np, MT = QR / 16;
-    const int KS = MT >= 4 ? 1 : 4 / MT;
-    const int n_keys = c->h_rows->n_keys;
-    const int n_chunks = (n_keys + ATT_KC - 1) / ATT_KC;
-    const size_t smem = (size_t)QR * ATT_LD * 2 + 2 * ATT_KC * ATT_LD * 2 + (size_t)np * c->ancw * 4;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
-                                         (double)n_chunks * KS * Hkv * QR * (hd + 2) * 4);
-    attn_mma_kernel<<<dim3(n_chunks, Hkv), 128, smem, c->st>>>(a);
-    prof_end(c, api);
-    CK_LAUNCH(c);
-    attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, n_chunks * KS);
-    CK_LAUNCH(c);
+    if ((rc = launch_attention(c, l))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
     e.x = c->x;
@@ -557,8 +616,13 @@ int layer_forward(fs_ctx* c, int l) {
         yf, (const float*)w.bqkv, c->rope, (float*)c->q, (float*)kv_plane(c, l, 0),
         (float*)kv_plane(c, l, 1), H, Hkv, hd, f.max_ctx, c->d_rows);
     CK_LAUNCH(c);
-    const int n_keys = c->h_rows->n_keys;
-    attn_simple_kernel<float><<<dim3(H, FS_MAX_SEG), 128, (size_t)n_keys * 4, c->st>>>(
+    static bool sattr = false;
+    if (!sattr) {
+      cudaFuncSetAttribute(attn_simple_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      sattr = true;
+    }
+    // scores for up to max_ctx keys (fixed size: the launch is graph-replayed)
+    attn_simple_kernel<float><<<dim3(H, FS_MAX_SEG), 128, (size_t)f.max_ctx * 4, c->st>>>(
         (const float*)c->q, (const float*)kv_plane(c, l, 0), (const float*)kv_plane(c, l, 1),
         (float*)c->att, c->d_rows, c->tree.anc, c->ancw, f.max_live, H, Hkv, hd, f.max_ctx,
         (float)(1.0 / std::sqrt((double)hd)));
@@ -627,13 +691,40 @@ int stage_forward(fs_ctx* c, bool from_hin) {
       embed_kernel<float><<<FS_MAX_SEG, 256, 0, c->st>>>((const float*)c->emb, d, c->d_rows, c->x);
     CK_LAUNCH(c);
   } else if (from_hin) {
-    CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)n * d * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)c->cfg.max_seg * d * 4, cudaMemcpyDeviceToDevice, c->st));
   }
   for (int l = 0; l < c->nl; l++) {
     int rc = layer_forward(c, l);
     if (rc) return rc;
   }
   if (c->last) return head_forward(c);
+  return FS_OK;
+}
+
+// the tick's stage forward: replay a captured CUDA graph (sizes live in
+// d_rows, so one graph serves every tick); direct launches when profiling
+int tick_forward(fs_ctx* c) {
+  if (!c->use_graph || c->prof) return stage_forward(c, true);
+  if (c->fwd_exec && c->fwd_logits != c->logits_buf) {
+    cudaGraphExecDestroy(c->fwd_exec);
+    c->fwd_exec = nullptr;
+  }
+  if (!c->fwd_exec) {
+    cudaGraph_t g;
+    const uint64_t l0 = c->launches;
+    CK_CUDA(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+    int rc = stage_forward(c, true);
+    cudaError_t e = cudaStreamEndCapture(c->st, &g);
+    if (rc) return rc;
+    CK_CUDA(c, e);
+    CK_CUDA(c, cudaGraphInstantiate(&c->fwd_exec, g, 0));
+    cudaGraphDestroy(g);
+    c->fwd_kernels = c->launches - l0;
+    c->launches = l0;
+    c->fwd_logits = c->logits_buf;
+  }
+  CK_CUDA(c, cudaGraphLaunch(c->fwd_exec, c->st));
+  c->launches += c->fwd_kernels;
   return FS_OK;
 }
 
@@ -697,6 +788,7 @@ int fs_init(const fs_config* cfg, fs_ctx** out) {
   }
   cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, cfg->device);
   c->st = (cudaStream_t)cfg->stream;
+  c->use_graph = getenv("FS_NO_GRAPH") == nullptr;
   const size_t need = carve(c, nullptr);
   if (cfg->arena_bytes < need) {
     delete c;
@@ -985,7 +1077,7 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     // host mirror of the sizes the launch configuration needs
     c->h_rows->n_rows = cur.n();
     c->h_rows->n_keys = c->l_glo + cur.e;
-    if ((rc = stage_forward(c, true))) return rc;
+    if ((rc = tick_forward(c))) return rc;
   }
   // stage transport: p -> p+1 hidden rows (fp32), NCCL over NVLink
   if (P > 1) {
@@ -1250,8 +1342,112 @@ int fs_get_profile(fs_ctx* c, fs_profile* out) {
   return FS_OK;
 }
 
+int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!c->weights || !c->prefixed || iters < 1 || !us || !bytes || kind < 0 || kind > 7)
+    return fail(c, FS_EINVAL, "bad bench request");
+  if (kind <= 5 && !c->bf) return fail(c, FS_EINVAL, "bf16 path only");
+  if (kind == 4 && !c->last) return fail(c, FS_EINVAL, "head lives on the last stage");
+  const fs_config& f = c->cfg;
+  LayerW& w = c->lw[0];
+  GemmEpi e = base_epi(c);
+  const GemmOp* g = nullptr;
+  switch (kind) {
+    case 0: g = &w.qkv; e.mode = EPI_QKV; e.bias = (const bf16*)w.bqkv; e.q_out = (bf16*)c->q;
+            e.k_cache = (bf16*)kv_plane(c, 0, 0); e.v_cache = (bf16*)kv_plane(c, 0, 1); break;
+    case 1: g = &w.o; e.mode = EPI_STORE; e.out = c->x; e.ldo = 0; break;
+    case 2: g = &w.gu; e.mode = EPI_GLU; e.act = (bf16*)c->act; break;
+    case 3: g = &w.dn; e.mode = EPI_STORE; e.out = c->x; e.ldo = 0; break;
+    case 4: g = &c->head; e.mode = EPI_HEAD; e.head_part = c->head_part; break;
+    default: break;
+  }
+  // EPI_STORE with ldo 0 writes row 0 only: benchmark without touching x rows
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double by = 0;
+  cudaEventRecord(a, c->st);
+  for (int i = 0; i < iters; i++) {
+    if (g) {
+      if ((rc = launch_gemm(c, *g, e))) return rc;
+      by = (double)g->sh.n_out * g->sh.K * 2;
+    } else if (kind == 5 || kind == 7) {
+      if (kind == 7) {
+        if ((rc = tick_forward(c))) return rc;
+      } else {
+        bool pr = c->prof;
+        c->prof = true;
+        size_t before = c->ev_used.size();
+        if ((rc = launch_attention(c, 0))) return rc;
+        by = c->ev_used.size() > before ? c->ev_used.back().second : 0;
+        c->ev_used.resize(before);
+        c->ev_next = before * 2;
+        c->prof = pr;
+      }
+    } else {
+      rmsnorm_kernel<bf16, bf16, true><<<c->npad, 256, 0, c->st>>>(c->x, (const bf16*)w.g1, (bf16*)c->y,
+                                                                   f.d_model, (float)f.rms_eps, c->d_rows);
+      CK_LAUNCH(c);
+      by = (double)c->h_rows->n_rows * f.d_model * 4;
+    }
+  }
+  cudaEventRecord(b, c->st);
+  CK_CUDA(c, cudaEventSynchronize(b));
+  if (g && getenv("FS_ATT_DEBUG")) {
+    const int ncta = 148;
+    cudaMalloc(&c->gemm_dbg, sizeof(unsigned long long) * 8 * ncta);
+    cudaMemsetAsync(c->gemm_dbg, 0, sizeof(unsigned long long) * 8 * ncta, c->st);
+    launch_gemm(c, *g, e);
+    std::vector<unsigned long long> h(8 * ncta);
+    cudaMemcpyAsync(h.data(), c->gemm_dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    unsigned long long t0 = ~0ull, tend = 0;
+    for (int i = 0; i < g->grid; i++) { t0 = std::min(t0, h[i * 8]); tend = std::max(tend, h[i * 8 + 6]); }
+    for (int k = 0; k < 7; k++) {
+      double sum = 0, mx = 0, mn = 1e30; int n = 0;
+      for (int i = 0; i < g->grid; i++)
+        if (h[i * 8 + k]) { double v = (h[i * 8 + k] - t0) / 1e3; sum += v; mx = std::max(mx, v); mn = std::min(mn, v); n++; }
+      if (n) fprintf(stderr, "gemm probe %d: min %7.2f mean %7.2f max %7.2f us (n=%d)\n", k, mn, sum / n, mx, n);
+    }
+    fprintf(stderr, "gemm kernel span %.2f us\n", (tend - t0) / 1e3);
+    cudaFree(c->gemm_dbg);
+    c->gemm_dbg = nullptr;
+  }
+  if (kind == 5 && getenv("FS_ATT_DEBUG")) {
+    // one more probed launch: per-phase times (us from CTA start), mean/max over CTAs
+    const int ncta = 8 * c->cfg.n_kv_heads;
+    if (!c->att_dbg) cudaMalloc(&c->att_dbg, sizeof(unsigned long long) * 16 * ncta);
+    cudaMemsetAsync(c->att_dbg, 0, sizeof(unsigned long long) * 16 * ncta, c->st);
+    launch_attention(c, 0);
+    std::vector<unsigned long long> h(16 * ncta);
+    cudaMemcpyAsync(h.data(), c->att_dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    unsigned long long t0 = ~0ull, tend = 0;
+    for (int i = 0; i < ncta; i++)
+      if (h[i * 16]) { t0 = std::min(t0, h[i * 16]); tend = std::max(tend, h[i * 16 + 14]); }
+    for (int k = 0; k < 15; k++) {
+      double sum = 0, mx = 0; int n = 0;
+      for (int i = 0; i < ncta; i++)
+        if (h[i * 16] && h[i * 16 + k]) { double v = (h[i * 16 + k] - t0) / 1e3; sum += v; mx = std::max(mx, v); n++; }
+      if (n) fprintf(stderr, "probe %2d: mean %7.2f us  max %7.2f us  (n=%d)\n", k, sum / n, mx, n);
+    }
+    fprintf(stderr, "kernel span %.2f us\n", (tend - t0) / 1e3);
+    cudaFree(c->att_dbg);
+    c->att_dbg = nullptr;
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *us = 1e3 * ms / iters;
+  *bytes = by;
+  return FS_OK;
+}
+
 void fs_destroy(fs_ctx* c) {
   if (!c) return;
+  if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_sub) cudaFreeHost(c->h_sub);

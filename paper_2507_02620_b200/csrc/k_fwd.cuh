@@ -4,9 +4,12 @@
 // the fp32 configuration), split combine, argmax/top-2, and the fp32
 // CUDA-core GEMM + epilogues used by the fp32 (no-TF32) configuration.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "state.cuh"
 
 namespace fs {
+
 
 // ---------------------------------------------------------------- embedding
 template <typename T>
@@ -175,7 +178,18 @@ struct AttnArgs {
   float* ws_ml;         // [n_chunk_cap][Hkv][QR][2]
   int ancw, max_live, H, Hkv, max_ctx, npad, n_chunk_cap;
   float scale_log2;     // log2(e) / sqrt(hd)
+  unsigned long long* dbg;  // optional phase timestamps [cta][16] (diagnostics)
 };
+FS_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATT_PROBE(k)                                                               \
+  do {                                                                             \
+    if (a.dbg && threadIdx.x == 0)                                                 \
+      a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();  \
+  } while (0)
 
 // block 128 threads (4 warps); dyn smem: Q [QR][LD] + K,V [KC][LD] + anc rows
 __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
@@ -192,7 +206,7 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
   bf16* sK = sQ + (size_t)QR * ATT_LD;
   bf16* sV = sK + ATT_KC * ATT_LD;
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(sV + ATT_KC * ATT_LD);  // [npad][ancw]
-  if (k0 >= nk || n_rows == 0) return;
+  if (k0 >= nk || n_rows == 0) return;   // grid is sized for max_ctx (graph replay)
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   // ---- stage Q (GQA-packed), K, V chunk, ancestor rows
   for (int idx = tid; idx < QR * (ATT_HD / 8); idx += 128) {
@@ -354,9 +368,10 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
 
 // merge the split partials: o = sum_c O_c 2^(m_c - M) / sum_c l_c 2^(m_c - M)
 // grid (npad, H), block 128 (one thread per head-dim element)
-__global__ void attn_combine_kernel(AttnArgs a, bf16* out, int n_parts) {
+__global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks) {
   const int m = blockIdx.x, h = blockIdx.y;
   if (m >= a.rows->n_rows) return;
+  const int n_parts = (a.rows->n_keys + ATT_KC - 1) / ATT_KC * ks;
   const int G = a.H / a.Hkv;
   const int kvh = h / G, g = h % G;
   const int QR = G * a.npad;
@@ -377,6 +392,306 @@ __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int n_parts) {
   const bf16 hi = __float2bfloat16_rn(o);
   out[((size_t)m * a.H + h) * ATT_HD + j] = hi;  // hi/lo activation pair
   out[((size_t)(a.npad + m) * a.H + h) * ATT_HD + j] = __float2bfloat16_rn(o - __bfloat162float(hi));
+}
+
+// ---------------------------------------------------------------- MHA attention
+// Segment rows x heads with G*npad <= 32 query rows per kv head (MHA configs).
+// CTA = (key split, kv head); the nsplit (<= 8) splits of one kv head form a
+// thread-block cluster.  Each CTA streams its keys through a ring of ATT_NBUF
+// 64-key cp.async sub-chunk buffers (all issued up front when they fit); each
+// m16 query tile is shared by KS = 4/MT warps taking KPW = 64/KS keys of every
+// sub-chunk with a running (m, l, O).  The KS warp states merge in shared
+// memory into one CTA partial; after a cluster barrier, CTA rank r merges rows
+// r, r+nsplit, ... of all splits through distributed shared memory (split
+// order: deterministic) and writes the bf16 hi/lo attention output pair.
+constexpr int ATT_SUB = 64;   // keys per sub-chunk
+constexpr int ATT_NBUF = 3;   // sub-chunk ring depth
+constexpr int ATT_MAXQR = 32;
+
+struct AttnMhaArgs {
+  AttnArgs a;
+  bf16* out;            // [2*npad][H*128] hi rows then lo rows
+};
+
+template <int KPW>
+__global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const AttnArgs& a = args.a;
+  extern __shared__ __align__(16) uint8_t att_smem[];
+  const int split = blockIdx.x, kvh = blockIdx.y, nsplit = gridDim.x;
+  const TickRows* rows = a.rows;
+  const int G = a.H / a.Hkv;
+  const int QR = G * a.npad;
+  const int MT = QR / 16;
+  constexpr int KS = ATT_SUB / KPW;
+  // smem: Q [QR][LD] | K/V ring [NBUF][K|V][SUB][LD] | ancestor rows [npad][ancw]
+  // after the key loop the ring is reused: key-warp states [4][16][HD] + [4][16][2],
+  // then the CTA partial [QR][HD] + [QR][2] read by the cluster peers
+  bf16* sQ = reinterpret_cast<bf16*>(att_smem);
+  bf16* sKV = sQ + (size_t)QR * ATT_LD;
+  uint32_t* sAnc = reinterpret_cast<uint32_t*>(sKV + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD);
+  float* sPart = reinterpret_cast<float*>(sKV) + 4 * 16 * ATT_HD + 4 * 16 * 2;
+  float* sPml = sPart + ATT_MAXQR * ATT_HD;
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  // keys of this split; rows/sizes are written before the tick's first kernel
+  const int nk = rows->n_keys;
+  // keys per split from the device-side sizes (graph-replayable launch)
+  const int per = (nk + nsplit * ATT_SUB - 1) / (nsplit * ATT_SUB) * ATT_SUB;
+  const int kbeg = min(nk, split * per);
+  const int kend = min(nk, kbeg + per);
+  const int nsc = kend > kbeg ? (kend - kbeg + ATT_SUB - 1) / ATT_SUB : 0;
+  const bf16* kbase = a.kc + ((size_t)kvh * a.max_ctx) * ATT_HD;
+  const bf16* vbase = a.vc + ((size_t)kvh * a.max_ctx) * ATT_HD;
+  auto load_sub = [&](int sc) {
+    bf16* dK = sKV + (size_t)(sc % ATT_NBUF) * 2 * ATT_SUB * ATT_LD;
+    bf16* dV = dK + ATT_SUB * ATT_LD;
+    const int k0 = kbeg + sc * ATT_SUB;
+    for (int idx = tid; idx < ATT_SUB * (ATT_HD / 8); idx += 128) {
+      const int r = idx / (ATT_HD / 8), c = idx % (ATT_HD / 8);
+      const int slot = min(k0 + r, a.max_ctx - 1);
+      cp_async16(dK + (size_t)r * ATT_LD + c * 8, kbase + (size_t)slot * ATT_HD + c * 8);
+      cp_async16(dV + (size_t)r * ATT_LD + c * 8, vbase + (size_t)slot * ATT_HD + c * 8);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // context K/V below the first slot written this tick do not depend on the
+  // previous kernel (PDL): stream them before the grid dependency resolves
+  ATT_PROBE(0);
+  const int first_written = rows->slot[0];
+  const int npre = min(nsc, ATT_NBUF);
+  int issued = 0;
+  while (issued < npre && kbeg + (issued + 1) * ATT_SUB <= first_written) load_sub(issued++);
+  pdl_wait();
+  const int n_rows = rows->n_rows;
+  // Q (GQA-packed rows) and the ancestor rows: one cp.async group
+  for (int idx = tid; idx < QR * (ATT_HD / 8); idx += 128) {
+    const int r = idx / (ATT_HD / 8), c = idx % (ATT_HD / 8);
+    const int g = r / a.npad, m = r % a.npad;
+    cp_async16(sQ + (size_t)r * ATT_LD + c * 8, a.q + ((size_t)m * a.H + kvh * G + g) * ATT_HD + c * 8);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int idx = tid; idx < a.npad * a.ancw; idx += 128) {
+    const int m = idx / a.ancw, w = idx % a.ancw;
+    const int s = (m < n_rows) ? rows->sidx[m] : -1;
+    sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
+  }
+  while (issued < npre) load_sub(issued++);
+  pdl_trigger();
+  ATT_PROBE(1);
+  const int mt = warp % MT, ks = warp / MT;
+  const int g_row = lane >> 2, t4 = lane & 3;
+  int qm[2], ctx[2], sl[2];
+  for (int h2 = 0; h2 < 2; h2++) {
+    const int r = mt * 16 + g_row + 8 * h2;
+    qm[h2] = r % a.npad;
+    ctx[h2] = (qm[h2] < n_rows) ? rows->ctx_lim[qm[h2]] : 0;
+    sl[h2] = (qm[h2] < n_rows) ? rows->sidx[qm[h2]] : -1;
+  }
+  const int l_glo = rows->l_glo;
+  float oacc[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; j++) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  constexpr int NT8 = KPW / 8;
+  // groups committed so far: pre-dependency sub-chunks, Q, remaining prefetch;
+  // wait until sub-chunk sc and Q have landed
+  for (int sc = 0; sc < nsc; sc++) {
+    const int pending_after = issued - 1 - sc;   // sub-chunk groups younger than sc
+    if (pending_after >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (pending_after == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    ATT_PROBE(2 + sc);
+    const bf16* sK = sKV + (size_t)(sc % ATT_NBUF) * 2 * ATT_SUB * ATT_LD;
+    const bf16* sV = sK + ATT_SUB * ATT_LD;
+    const int kb = ks * KPW;
+    const int key0 = kbeg + sc * ATT_SUB + kb;
+    float sacc[NT8][4];
+#pragma unroll
+    for (int j = 0; j < NT8; j++) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < ATT_HD / 16; kk++) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4(a0, a1, a2, a3, sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
+#pragma unroll
+      for (int j = 0; j < NT8; j++) {
+        uint32_t b0, b1;
+        ldsm_x2(b0, b1, sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8);
+        mma_bf16_16816(sacc[j], a0, a1, a2, a3, b0, b1);
+      }
+    }
+    float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int j = 0; j < NT8; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int h2 = e >> 1;
+        const int key = key0 + j * 8 + t4 * 2 + (e & 1);
+        bool vis = key < kend && qm[h2] < n_rows;
+        if (vis && key >= ctx[h2]) {
+          const int aa = key - l_glo;
+          vis = sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
+                ((sAnc[qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+        }
+        const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
+        sacc[j][e] = v;
+        mnew[h2] = fmaxf(mnew[h2], v);
+      }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) {
+      mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 1));
+      mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 2));
+    }
+    float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) {
+      corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : exp2f(mrow[h2] - mnew[h2]);
+      mrow[h2] = mnew[h2];
+    }
+#pragma unroll
+    for (int j = 0; j < NT8; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int h2 = e >> 1;
+        const float p = (sacc[j][e] == -INFINITY) ? 0.f : exp2f(sacc[j][e] - mrow[h2]);
+        sacc[j][e] = p;
+        rs[h2] += p;
+      }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; h2++) lrow[h2] = lrow[h2] * corr[h2] + rs[h2];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      oacc[j][0] *= corr[0];
+      oacc[j][1] *= corr[0];
+      oacc[j][2] *= corr[1];
+      oacc[j][3] *= corr[1];
+    }
+    // O += P V with P as a bf16 hi + lo pair (R18: fp32 softmax/accumulation)
+#pragma unroll
+    for (int kk = 0; kk < KPW / 16; kk++) {
+      uint32_t ph[4], pl[4];
+#pragma unroll
+      for (int f = 0; f < 4; f++) {
+        const int jt = 2 * kk + (f >> 1), e0 = (f & 1) * 2;
+        const float x0 = sacc[jt][e0], x1 = sacc[jt][e0 + 1];
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+        ph[f] = *reinterpret_cast<const uint32_t*>(&h);
+        pl[f] = pack_bf16(x0 - __bfloat162float(h.x), x1 - __bfloat162float(h.y));
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        uint32_t b0, b1;
+        ldsm_x2_t(b0, b1, sV + (size_t)(kb + kk * 16 + (lane & 15)) * ATT_LD + j * 8);
+        mma_bf16_16816(oacc[j], ph[0], ph[1], ph[2], ph[3], b0, b1);
+        mma_bf16_16816(oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
+      }
+    }
+    __syncthreads();                                    // ring slot sc free
+    if (issued < nsc) load_sub(issued++);
+  }
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) {
+    lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 1);
+    lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 2);
+  }
+  ATT_PROBE(10);
+  // ---- merge the KS key-warps of each m-tile (shared memory)
+  float* so = reinterpret_cast<float*>(sKV);                  // [4][16][HD]
+  float* sml = so + 4 * 16 * ATT_HD;                          // [4][16][2]
+  __syncthreads();
+  for (int h2 = 0; h2 < 2; h2++) {
+    const int r16 = g_row + 8 * h2;
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+      *reinterpret_cast<float2*>(so + ((size_t)warp * 16 + r16) * ATT_HD + j * 8 + t4 * 2) =
+          make_float2(oacc[j][2 * h2], oacc[j][2 * h2 + 1]);
+    if (t4 == 0) {
+      sml[(warp * 16 + r16) * 2] = mrow[h2];
+      sml[(warp * 16 + r16) * 2 + 1] = lrow[h2];
+    }
+  }
+  __syncthreads();
+  // 8 threads per row, 16 head dims (4 x float4) each; KS <= 4 unrolled
+  for (int r = tid >> 3; r < QR; r += 16) {
+    const int m2 = r / 16, r16 = r % 16, d0 = (tid & 7) * 16;
+    float mm[KS], M = -INFINITY;
+#pragma unroll
+    for (int k2 = 0; k2 < KS; k2++) {
+      mm[k2] = sml[((m2 + MT * k2) * 16 + r16) * 2];
+      M = fmaxf(M, mm[k2]);
+    }
+    float L = 0.f;
+    float4 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k2 = 0; k2 < KS; k2++) {
+      const int w = m2 + MT * k2;
+      const float wt = (mm[k2] == -INFINITY) ? 0.f : exp2f(mm[k2] - M);
+      L += sml[(w * 16 + r16) * 2 + 1] * wt;
+      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)w * 16 + r16) * ATT_HD + d0);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const float4 o = src[u];
+        acc[u].x += o.x * wt;
+        acc[u].y += o.y * wt;
+        acc[u].z += o.z * wt;
+        acc[u].w += o.w * wt;
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(sPart + r * ATT_HD + d0);
+#pragma unroll
+    for (int u = 0; u < 4; u++) dst[u] = acc[u];
+    if ((tid & 7) == 0) {
+      sPml[r * 2] = M;
+      sPml[r * 2 + 1] = L;
+    }
+  }
+  // ---- cluster merge of the splits through distributed shared memory:
+  // CTA rank r owns rows r, r+nsplit, ...; 32 threads (float4 each) per row
+  ATT_PROBE(11);
+  cluster.sync();
+  ATT_PROBE(12);
+  const int crank = (int)cluster.block_rank();
+  for (int rr = crank + nsplit * (tid >> 5); rr < QR; rr += nsplit * 4) {
+    const int m = rr % a.npad, g = rr / a.npad;
+    if (m >= n_rows) continue;
+    const int q4 = (tid & 31) * 4;
+    float mm[8], M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      mm[c] = -INFINITY;
+      if (c < nsplit) mm[c] = cluster.map_shared_rank(sPml, c)[rr * 2];
+      M = fmaxf(M, mm[c]);
+    }
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      if (c < nsplit && mm[c] != -INFINITY) {
+        const float wt = exp2f(mm[c] - M);
+        L += cluster.map_shared_rank(sPml, c)[rr * 2 + 1] * wt;
+        const float4 o = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sPart, c) + rr * ATT_HD + q4);
+        acc.x += o.x * wt;
+        acc.y += o.y * wt;
+        acc.z += o.z * wt;
+        acc.w += o.w * wt;
+      }
+    }
+    const float v[4] = {acc.x / L, acc.y / L, acc.z / L, acc.w / L};
+    const size_t base = ((size_t)m * a.H + kvh * G + g) * ATT_HD + q4;
+    const size_t lob = ((size_t)(a.npad + m) * a.H + kvh * G + g) * ATT_HD + q4;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const bf16 hi = __float2bfloat16_rn(v[u]);
+      args.out[base + u] = hi;
+      args.out[lob + u] = __float2bfloat16_rn(v[u] - __bfloat162float(hi));
+    }
+  }
+  ATT_PROBE(13);
+  cluster.sync();   // keep every CTA's shared memory alive until all reads are done
+  ATT_PROBE(14);
 }
 
 // ---------------------------------------------------------------- argmax

@@ -31,7 +31,17 @@ struct GemmShape {
   int n_out, K, kb_total, n_tiles, units, max_contrib;
   float* ws;       // [n_tiles][max_contrib][128][NT] fp32 partials
   int* counters;   // [n_tiles], zero between launches
+  unsigned long long* dbg;  // optional phase timestamps [cta][8] (diagnostics)
 };
+FS_DEV unsigned long long g_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GEMM_PROBE(k)                                        \
+  do {                                                       \
+    if (sh.dbg) sh.dbg[(size_t)blockIdx.x * 8 + (k)] = g_gtimer(); \
+  } while (0)
 
 struct GemmEpi {
   int mode;
@@ -68,8 +78,13 @@ struct GemmCfg {
   static constexpr int A_BYTES = 128 * 64 * 2;           // 16 KB weight tile
   static constexpr int B_BYTES = BN * 64 * 2;            // activation tile (hi|lo)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = NT <= 16 ? 9 : (NT <= 32 ? 8 : 5);
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  // NT=16: 5 stages -> ~110 KB, two CTAs per SM (the next GEMM's CTA starts
+  // streaming its weights while this one drains: early PDL trigger)
+  static constexpr int STAGES = NT <= 16 ? 5 : (NT <= 32 ? 4 : 3);
+  static constexpr int MIN_CTAS = NT <= 16 ? 2 : 1;
+  // two accumulator buffers (segment s uses buffer s&1) so the MMA of the next
+  // tile segment never waits for the epilogue of the previous one
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int XCH_BYTES = 128 * (NT + 1) * 4;
   static constexpr int TOP_BYTES = 4 * NT * (int)sizeof(Top2);
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + XCH_BYTES + TOP_BYTES;
@@ -165,7 +180,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 }
 
 template <int NT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    GemmShape sh, GemmEpi ep) {
   using C = GemmCfg<NT>;
@@ -175,9 +190,9 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* acc_full = empty + C::STAGES;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_full = empty + C::STAGES;      // [2]
+  uint64_t* acc_empty = acc_full + 2;          // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
   int* s_flag = reinterpret_cast<int*>(tmem_holder + 1);
   float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   Top2* stop = reinterpret_cast<Top2*>(reinterpret_cast<uint8_t*>(xch) + C::XCH_BYTES);
@@ -187,6 +202,7 @@ __global__ void __launch_bounds__(192, 1)
   const int U = sh.units, KB = sh.kb_total;
   const int u0 = (int)((long long)c * U / G), u1 = (int)((long long)(c + 1) * U / G);
 
+  if (threadIdx.x == 0) GEMM_PROBE(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -194,15 +210,21 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
+    for (int b = 0; b < 2; b++) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
     fence_barrier_init();
   }
+  __syncwarp();
   if (warp == 1) tmem_alloc(tmem_holder, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // dependents may launch now: they prefetch their weights and wait on
+  // griddepcontrol.wait (full completion of this grid) before reading outputs
+  pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer: weights never depend on the previous
@@ -218,7 +240,9 @@ __global__ void __launch_bounds__(192, 1)
         mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
         tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (u % KB) * 64, (u / KB) * 128, polA);
       }
+      GEMM_PROBE(1);
       pdl_wait();  // activations (B) are produced by the previous kernel
+      GEMM_PROBE(2);
       for (int i = 0; i < pre; i++) {
         const int u = u0 + i;
         tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (u % KB) * 64, 0, polB);
@@ -236,6 +260,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread)
     if (lane == 0) {
@@ -246,16 +271,19 @@ __global__ void __launch_bounds__(192, 1)
       while (u < u1) {
         const int t = u / KB;
         const int seg_start = u, seg_end = min(u1, (t + 1) * KB);
-        if (seg > 0) mbar_wait(acc_empty, (seg - 1) & 1);
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&acc_empty[buf], ((seg >> 1) - 1) & 1);
         tc_fence_after();
+        const uint32_t tacc = tmem + (uint32_t)(buf * C::BN);
         for (; u < seg_end; u++) {
           mbar_wait(&full[stage], phase);
+          if (u == u0) GEMM_PROBE(3);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < 4; k++)
-            umma_bf16(tmem, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
+            umma_bf16(tacc, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
                       (u > seg_start || k > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
@@ -263,10 +291,12 @@ __global__ void __launch_bounds__(192, 1)
             phase ^= 1;
           }
         }
-        umma_commit(acc_full);
+        umma_commit(&acc_full[buf]);
         seg++;
       }
+      GEMM_PROBE(4);
     }
+    __syncwarp();
   } else {
     // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
     const int q = warp & 3;
@@ -275,10 +305,11 @@ __global__ void __launch_bounds__(192, 1)
     while (u < u1) {
       const int t = u / KB;
       const int seg_start = u, seg_end = min(u1, (t + 1) * KB);
-      mbar_wait(acc_full, seg & 1);
+      const int buf = seg & 1;
+      mbar_wait(&acc_full[buf], (seg >> 1) & 1);
       tc_fence_after();
       float v[NT];
-      const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+      const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
 #pragma unroll
       for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
 #pragma unroll
@@ -289,7 +320,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = 0; i < 16; i++) v[j + i] += w[i];
       }
       tc_fence_before();
-      mbar_arrive(acc_empty);
+      mbar_arrive(&acc_empty[buf]);
       const bool whole = (seg_start == t * KB) && (seg_end == (t + 1) * KB);
       bool run_epi = whole;
       if (!whole) {
@@ -329,8 +360,9 @@ __global__ void __launch_bounds__(192, 1)
       seg++;
     }
   }
+  if (threadIdx.x == 64) GEMM_PROBE(5);
   __syncthreads();
-  pdl_trigger();
+  if (threadIdx.x == 0) GEMM_PROBE(6);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
