@@ -1445,6 +1445,52 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
   return FS_OK;
 }
 
+int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32_t n, float* Y) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (!c->bf || !c->weights || !X || !Y || n < 1 || n > c->cfg.max_seg || which < 0 || which > 4 ||
+      layer < c->L0 || layer >= c->L1 || (which == 4 && !c->last))
+    return fail(c, FS_EINVAL, "bad debug gemm request");
+  LayerW& w = c->lw[layer - c->L0];
+  const GemmOp* g = which == 0 ? &w.qkv : which == 1 ? &w.o : which == 2 ? &w.gu : which == 3 ? &w.dn : &c->head;
+  const int K = g->sh.K, N = g->sh.n_out, np = c->npad;
+  // hi/lo bf16 pair of X into the B-operand buffer of this GEMM
+  void* bbuf = (which == 1) ? c->att : (which == 3) ? c->act : c->y;
+  std::vector<uint16_t> hb((size_t)2 * np * K, 0);
+  for (int m = 0; m < n; m++)
+    for (int k = 0; k < K; k++) {
+      float v = X[(size_t)m * K + k];
+      uint32_t u;
+      memcpy(&u, &v, 4);
+      uint32_t hi = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+      float hf;
+      memcpy(&hf, &hi, 4);
+      float lo = v - hf;
+      uint32_t ul;
+      memcpy(&ul, &lo, 4);
+      uint32_t lob = (ul + 0x7fffu + ((ul >> 16) & 1u)) & 0xffff0000u;
+      hb[(size_t)m * K + k] = (uint16_t)(hi >> 16);
+      hb[(size_t)(np + m) * K + k] = (uint16_t)(lob >> 16);
+    }
+  CK_CUDA(c, cudaMemcpyAsync(bbuf, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice, c->st));
+  c->h_rows->n_rows = n;
+  c->h_rows->n_keys = 1;
+  if ((rc = upload_rows(c))) return rc;
+  float* out = nullptr;
+  CK_CUDA(c, cudaMalloc(&out, sizeof(float) * (size_t)n * N));
+  GemmEpi e = base_epi(c);
+  e.mode = EPI_STORE;
+  e.out = out;
+  e.ldo = N;
+  rc = launch_gemm(c, *g, e);
+  if (!rc) {
+    cudaMemcpyAsync(Y, out, sizeof(float) * (size_t)n * N, cudaMemcpyDeviceToHost, c->st);
+    rc = sync(c);
+  }
+  cudaFree(out);
+  return rc;
+}
+
 void fs_destroy(fs_ctx* c) {
   if (!c) return;
   if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);

@@ -62,7 +62,7 @@ class fs_profile(C.Structure):
                 ("attn_launches", C.c_uint64), ("attn_ms", C.c_double), ("attn_bytes", C.c_double)]
 
 
-EXPORTS = ["fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
+EXPORTS = ["fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
            "fs_last_error", "fs_strerror"]
@@ -97,6 +97,7 @@ def lib():
         L.fs_set_profiling.argtypes = [P, i32]
         L.fs_get_profile.argtypes = [P, C.POINTER(fs_profile)]
         L.fs_bench_kernel.argtypes = [P, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.fs_debug_gemm.argtypes = [P, i32, i32, C.POINTER(C.c_float), i32, C.POINTER(C.c_float)]
         L.fs_destroy.argtypes = [P]
         L.fs_last_error.restype = C.c_char_p
         L.fs_last_error.argtypes = [P]
@@ -285,6 +286,13 @@ class Pipeline:
         us, by = C.c_double(), C.c_double()
         self._chk(self.L.fs_bench_kernel(self.h, kind, iters, C.byref(us), C.byref(by)), "fs_bench_kernel")
         return us.value, by.value
+
+    def debug_gemm(self, layer, which, X, n_out):
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        Y = np.zeros((X.shape[0], n_out), np.float32)
+        self._chk(self.L.fs_debug_gemm(self.h, layer, which, X.ctypes.data_as(C.POINTER(C.c_float)),
+                                       X.shape[0], Y.ctypes.data_as(C.POINTER(C.c_float))), "fs_debug_gemm")
+        return Y
 
     def read_kv(self, layer, which, kvh, slot):
         out = np.zeros(self.shape.head_dim, np.float32)

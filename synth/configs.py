@@ -48,6 +48,9 @@ SHAPES = {
     # small bf16 shapes with head_dim 128 (same kernels as 7B/72B, seconds on CPU)
     "small": Shape(2, 512, 4, 4, 128, 1024, 1024, 0, 1, 1e-5, 1e4),
     "smallq": Shape(2, 1024, 8, 2, 128, 1536, 2048, 1, 1, 1e-6, 1e6),
+    # full per-layer shapes of 7B / 72B with 2 layers (oracle-cheap parity)
+    "7b_l2": Shape(2, 4096, 32, 32, 128, 11008, 32000, 0, 1, 1e-5, 1e4),
+    "72b_l2": Shape(2, 8192, 64, 8, 128, 29568, 152064, 1, 1, 1e-6, 1e6),
 }
 
 
