@@ -7,7 +7,8 @@
  *   residual x ............ fp32
  *   q, k, v (after bias+RoPE) bf16 (K/V cache storage)
  *   RMSNorm output, attention output, silu(g)*u (the GEMM inputs):
- *                           fp32 carried as bf16 hi + bf16 lo
+ *                           fp32 carried as bf16 hi + bf16 lo; an RMSNorm feeding
+ *                           a linear layer is applied as inv * (W (x*g))
  *   logits ................ fp32
  * (fp32 config: fp32 everywhere)
  * Compile with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
@@ -344,9 +345,13 @@ static double store_act2(const fso_cfg* c, double v) {
   return (double)hi + (double)lo;
 }
 
-/* y[m] = round(x[m] * rsqrt(mean(x[m]^2) + eps) * g)   (RMSNorm, LLaMA) */
+/* RMSNorm (LLaMA): RMSNorm(x) = x * inv * g with inv = 1/sqrt(mean(x^2) + eps).
+ * fp32 configs: y = fp32(x * inv * g), scale = 1.
+ * bf16 configs (R18): the norm feeds a linear layer, and
+ * W (x * inv * g) = inv * (W (x * g)); the GEMM input is y = hi/lo pair of
+ * fp32(x * g) and the linear output is multiplied by scale = inv afterwards. */
 static void rmsnorm(fso_model* m, int32_t layer, int32_t which, int32_t n_rows,
-                    const float* x, double* y) {
+                    const float* x, double* y, double* scale) {
   const fso_cfg* c = &m->c;
   int32_t d = c->d_model;
   float* g = (float*)malloc((size_t)d * 4);
@@ -355,10 +360,22 @@ static void rmsnorm(fso_model* m, int32_t layer, int32_t which, int32_t n_rows,
     double ss = 0.0;
     for (int32_t k = 0; k < d; k++) ss += (double)x[(int64_t)r * d + k] * (double)x[(int64_t)r * d + k];
     double inv = 1.0 / sqrt(ss / d + c->rms_eps);
-    for (int32_t k = 0; k < d; k++)
-      y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * inv * (double)g[k]);
+    if (c->bf16) {
+      scale[r] = inv;
+      for (int32_t k = 0; k < d; k++)
+        y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * (double)g[k]);
+    } else {
+      scale[r] = 1.0;
+      for (int32_t k = 0; k < d; k++)
+        y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * inv * (double)g[k]);
+    }
   }
   free(g);
+}
+
+static void scale_rows(double* out, int32_t n_rows, int64_t n_cols, const double* scale) {
+  for (int32_t r = 0; r < n_rows; r++)
+    for (int64_t j = 0; j < n_cols; j++) out[(int64_t)r * n_cols + j] *= scale[r];
 }
 
 /* out[m][r] = sum_k W[r][k] * in[m][k]  (fp64 accumulation, k ascending) */
@@ -442,13 +459,17 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
   double* u = (double*)malloc((size_t)n_rows * c->ffn * 8);
   double* o = (double*)malloc((size_t)n_rows * wmax * 8);
   float* bias = (float*)malloc((size_t)nq * 4);
+  double* rs = (double*)malloc((size_t)n_rows * 8);
 
   for (int32_t l = layer_begin; l < layer_end; l++) {
     /* --- self-attention block --- */
-    rmsnorm(m, l, FSO_ATTN_NORM, n_rows, x, y);
+    rmsnorm(m, l, FSO_ATTN_NORM, n_rows, x, y, rs);
     linear(m, l, FSO_Q, n_rows, y, q);
     linear(m, l, FSO_K, n_rows, y, kk);
     linear(m, l, FSO_V, n_rows, y, vv);
+    scale_rows(q, n_rows, nq, rs);
+    scale_rows(kk, n_rows, nkv, rs);
+    scale_rows(vv, n_rows, nkv, rs);
     if (c->qkv_bias) {
       get_row(m, l, FSO_BQ, 0, bias);
       for (int32_t r = 0; r < n_rows; r++)
@@ -510,9 +531,11 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
     for (int64_t i = 0; i < (int64_t)n_rows * d; i++) x[i] = (float)((double)x[i] + o[i]);
 
     /* --- SwiGLU FFN block --- */
-    rmsnorm(m, l, FSO_MLP_NORM, n_rows, x, y);
+    rmsnorm(m, l, FSO_MLP_NORM, n_rows, x, y, rs);
     linear(m, l, FSO_GATE, n_rows, y, g);
     linear(m, l, FSO_UP, n_rows, y, u);
+    scale_rows(g, n_rows, c->ffn, rs);
+    scale_rows(u, n_rows, c->ffn, rs);
     for (int64_t i = 0; i < (int64_t)n_rows * c->ffn; i++) {
       double gv = g[i];
       g[i] = store_act2(c, gv / (1.0 + exp(-gv)) * u[i]);
@@ -523,15 +546,17 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
 
   if (h_out) memcpy(h_out, x, (size_t)n_rows * d * 4);
   if (layer_end == c->n_layers && logits) {
-    rmsnorm(m, 0, FSO_FINAL_NORM, n_rows, x, y);
+    rmsnorm(m, 0, FSO_FINAL_NORM, n_rows, x, y, rs);
     int64_t V = c->vocab;
     double* lg = (double*)malloc((size_t)n_rows * V * 8);
     linear(m, 0, FSO_HEAD, n_rows, y, lg);
+    scale_rows(lg, n_rows, V, rs);
     for (int64_t i = 0; i < (int64_t)n_rows * V; i++) logits[i] = (float)lg[i];
     free(lg);
   }
   free(x); free(y); free(q); free(kk); free(vv); free(att); free(g); free(u); free(o);
   free(bias);
+  free(rs);
   return 0;
 }
 

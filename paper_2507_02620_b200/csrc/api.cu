@@ -54,7 +54,7 @@ struct Seg {
 };
 
 struct GemmOp {
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb;   // weights, bf16 hi/lo activations
   GemmShape sh;
   int grid = 0;
   bool ok = false;
@@ -91,6 +91,7 @@ struct fs_ctx {
   float *x = nullptr, *hin = nullptr, *yf = nullptr;
   void *y = nullptr, *q = nullptr, *att = nullptr, *act = nullptr;
   float *gws = nullptr;
+  float* ssq = nullptr;   // [d/128][npad] per-tile sums of squares of the residual
   int* gcnt = nullptr;
   Top2* head_part = nullptr;
   RowResult* res = nullptr;
@@ -99,6 +100,8 @@ struct fs_ctx {
   int* att_cnt = nullptr;
   unsigned long long* att_dbg = nullptr;  // FS_ATT_DEBUG diagnostics only
   unsigned long long* gemm_dbg = nullptr;
+  unsigned long long* tl_buf = nullptr;     // timeline diagnostics (fs_bench_kernel kind 8)
+  std::vector<std::string> tl_names;
   // CUDA graph of one tick's stage forward (replayed every tick)
   cudaGraphExec_t fwd_exec = nullptr;
   uint64_t fwd_kernels = 0;
@@ -318,6 +321,7 @@ size_t carve(fs_ctx* c, char* base) {
   c->gws_floats = wsf;
   c->gws = c->bf ? cv.take<float>(wsf) : nullptr;
   c->gcnt = cv.take<int>(max_tiles);
+  c->ssq = cv.take<float>((size_t)((d + 127) / 128) * np);
   c->head_part = cv.take<Top2>((size_t)((V + 127) / 128) * np);
   c->res = cv.take<RowResult>(FS_MAX_SEG);
   c->out_node = cv.take<int32_t>(FS_MAX_SEG);
@@ -372,15 +376,16 @@ bool setup_ctx(fs_ctx* c, const fs_config* f) {
 }
 
 bool encode_map(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                uint32_t box_outer) {
+                uint32_t box_outer, bool f32 = false) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
+  cuuint64_t strides[1] = {inner * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims,
+             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             f32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -398,11 +403,13 @@ bool build_maps(fs_ctx* c) {
     ok &= encode_map(&w.gu.tb, c->y, d, 2 * np, 64, 2 * np);
     ok &= encode_map(&w.dn.ta, w.wd, ffn, d, 64, 128);
     ok &= encode_map(&w.dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
+
     w.qkv.ok = w.o.ok = w.gu.ok = w.dn.ok = ok;
   }
   if (c->last) {
     ok &= encode_map(&c->head.ta, c->wh, d, f.vocab, 64, 128);
     ok &= encode_map(&c->head.tb, c->y, d, 2 * np, 64, 2 * np);
+
     c->head.ok = ok;
   }
   return ok;
@@ -443,9 +450,13 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   sh.ws = c->gws;
   sh.counters = c->gcnt;
   sh.dbg = c->gemm_dbg;
+  if (c->tl_buf) {
+    sh.dbg = c->tl_buf + c->tl_names.size() * 4096;
+    c->tl_names.push_back("gemm");
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(g.grid);
-  lc.blockDim = dim3(192);
+  lc.blockDim = dim3(GemmCfg<NT>::THREADS);
   lc.dynamicSmemBytes = GemmCfg<NT>::SMEM;
   lc.stream = c->st;
   cudaLaunchAttribute at[1];
@@ -486,6 +497,25 @@ GemmEpi base_epi(fs_ctx* c) {
   return e;
 }
 
+// epilogue params of a GEMM fed by an RMSNorm applied by linearity: B = (x*g)
+// as a hi/lo pair (written by the producer of x), accumulator rows *= inv[m]
+GemmEpi norm_input(fs_ctx* c) {
+  GemmEpi e = base_epi(c);
+  e.scale_ssq = c->ssq;
+  e.scale_n = c->cfg.d_model / 128;
+  e.eps = (float)c->cfg.rms_eps;
+  return e;
+}
+
+// the gain of the RMSNorm that follows local layer l's residual update
+// (down-proj): next layer's attention norm, the final norm, or none at a
+// stage boundary (the next stage prepares its own input)
+const bf16* next_gain_after_down(fs_ctx* c, int l) {
+  if (l + 1 < c->nl) return (const bf16*)c->lw[l + 1].g1;
+  if (c->last) return (const bf16*)c->gf;
+  return nullptr;
+}
+
 char* kv_plane(fs_ctx* c, int local_layer, int which) {
   return c->kv + ((size_t)local_layer * 2 + which) * c->kv_plane_elems * c->esz;
 }
@@ -512,6 +542,10 @@ int launch_attention(fs_ctx* c, int l) {
     a.n_chunk_cap = c->att_chunk_cap;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
     a.dbg = c->att_dbg;
+    if (c->tl_buf) {
+      a.dbg = c->tl_buf + c->tl_names.size() * 4096;
+      c->tl_names.push_back("attn");
+    }
     const int G = H / Hkv, QR = G * np, MT = QR / 16;
     const int KS = MT >= 4 ? 1 : 4 / MT;
     const int n_keys = c->h_rows->n_keys;
@@ -578,10 +612,8 @@ int layer_forward(fs_ctx* c, int l) {
   const int nq = (H + 2 * Hkv) * hd;
   int rc;
   if (c->bf) {
-    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)w.g1, (bf16*)c->y, d,
-                                                     (float)f.rms_eps, c->d_rows);
-    CK_LAUNCH(c);
-    GemmEpi e = base_epi(c);
+    // RMSNorm fused into the GEMM B operand (norm_input): no separate launch
+    GemmEpi e = norm_input(c);
     e.mode = EPI_QKV;
     e.bias = (const bf16*)w.bqkv;
     e.q_out = (bf16*)c->q;
@@ -592,17 +624,21 @@ int layer_forward(fs_ctx* c, int l) {
     e = base_epi(c);
     e.mode = EPI_RESID;
     e.x = c->x;
+    e.ssq_out = c->ssq;
+    e.z_gain = (const bf16*)w.g2;
+    e.z_out = (bf16*)c->y;
     if ((rc = launch_gemm(c, w.o, e))) return rc;
-    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)w.g2, (bf16*)c->y, d,
-                                                     (float)f.rms_eps, c->d_rows);
-    CK_LAUNCH(c);
-    e = base_epi(c);
+    e = norm_input(c);
     e.mode = EPI_GLU;
     e.act = (bf16*)c->act;
     if ((rc = launch_gemm(c, w.gu, e))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
     e.x = c->x;
+    const bf16* gn = next_gain_after_down(c, l);
+    e.ssq_out = gn ? c->ssq : nullptr;
+    e.z_gain = gn;
+    e.z_out = gn ? (bf16*)c->y : nullptr;
     if ((rc = launch_gemm(c, w.dn, e))) return rc;
   } else {
     float* yf = c->yf;
@@ -655,10 +691,7 @@ int head_forward(fs_ctx* c) {
   const fs_config& f = c->cfg;
   const int d = f.d_model, V = f.vocab, np = c->npad;
   if (c->bf) {
-    rmsnorm_kernel<bf16, bf16, true><<<np, 256, 0, c->st>>>(c->x, (const bf16*)c->gf, (bf16*)c->y, d,
-                                                     (float)f.rms_eps, c->d_rows);
-    CK_LAUNCH(c);
-    GemmEpi e = base_epi(c);
+    GemmEpi e = norm_input(c);
     e.mode = EPI_HEAD;
     e.head_part = c->head_part;
     e.logits = c->logits_buf;
@@ -692,6 +725,11 @@ int stage_forward(fs_ctx* c, bool from_hin) {
     CK_LAUNCH(c);
   } else if (from_hin) {
     CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)c->cfg.max_seg * d * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
+  if (c->bf) {  // first RMSNorm's inputs: per-128-column sums of squares and x*g (hi/lo)
+    const bf16* g0 = c->nl > 0 ? (const bf16*)c->lw[0].g1 : (const bf16*)c->gf;
+    norm_prep_kernel<<<c->npad, 128, 0, c->st>>>(c->x, g0, (bf16*)c->y, c->ssq, d, c->d_rows);
+    CK_LAUNCH(c);
   }
   for (int l = 0; l < c->nl; l++) {
     int rc = layer_forward(c, l);
@@ -1345,6 +1383,58 @@ int fs_get_profile(fs_ctx* c, fs_profile* out) {
 int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
   int rc;
   if (!check(c, &rc)) return rc;
+  if (kind == 8) {
+    // timeline of one (non-graph) stage forward: per probed launch, first CTA start and last
+    // CTA end relative to the first launch's start
+    const size_t per = 4096, nl = 400;
+    CK_CUDA(c, cudaMalloc(&c->tl_buf, per * nl * 8));
+    cudaMemsetAsync(c->tl_buf, 0, per * nl * 8, c->st);
+    c->tl_names.clear();
+    rc = stage_forward(c, false);
+    std::vector<unsigned long long> h(per * nl);
+    cudaMemcpyAsync(h.data(), c->tl_buf, h.size() * 8, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    cudaFree(c->tl_buf);
+    c->tl_buf = nullptr;
+    unsigned long long t00 = 0;
+    double prev_end = 0;
+    for (size_t i = 0; i < c->tl_names.size() && i < nl; i++) {
+      unsigned long long st = ~0ull, en = 0;
+      const bool g = c->tl_names[i] == "gemm";
+      for (size_t k = 0; k < per; k++) {
+        unsigned long long v = h[i * per + k];
+        if (!v) continue;
+        const size_t slot = g ? (k % 8) : (k % 16);
+        if (slot == 0) st = std::min(st, v);
+        en = std::max(en, v);
+      }
+      if (st == ~0ull) continue;
+      if (!t00) t00 = st;
+      const double s0 = (st - t00) / 1e3, e0 = (en - t00) / 1e3;
+      if (i < 24 || i + 3 >= c->tl_names.size()) {
+        fprintf(stderr, "%3zu %-5s start %8.2f end %8.2f dur %6.2f gap-from-prev-end %6.2f\n", i,
+                c->tl_names[i].c_str(), s0, e0, e0 - s0, s0 - prev_end);
+        if (g && i >= 3 && i <= 5) {  // per-probe distribution over CTAs for one layer
+          for (int k = 0; k < 7; k++) {
+            std::vector<double> vals;
+            for (size_t cta = 0; cta < 148; cta++) {
+              unsigned long long v = h[i * per + cta * 8 + k];
+              if (v) vals.push_back((v - t00) / 1e3);
+            }
+            if (vals.empty()) continue;
+            std::sort(vals.begin(), vals.end());
+            fprintf(stderr, "      probe %d: min %8.2f p10 %8.2f med %8.2f p90 %8.2f max %8.2f\n", k, vals[0],
+                    vals[vals.size() / 10], vals[vals.size() / 2], vals[vals.size() * 9 / 10], vals.back());
+          }
+        }
+      }
+      prev_end = e0;
+    }
+    c->tl_names.clear();
+    *us = prev_end;
+    *bytes = 0;
+    return rc;
+  }
   if (!c->weights || !c->prefixed || iters < 1 || !us || !bytes || kind < 0 || kind > 7)
     return fail(c, FS_EINVAL, "bad bench request");
   if (kind <= 5 && !c->bf) return fail(c, FS_EINVAL, "bf16 path only");

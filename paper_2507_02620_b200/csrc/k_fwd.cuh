@@ -20,6 +20,30 @@ __global__ void embed_kernel(const T* __restrict__ E, int d, const TickRows* row
   for (int k = threadIdx.x; k < d; k += blockDim.x) x[(size_t)m * d + k] = to_f32(E[tok * d + k]);
 }
 
+// First RMSNorm input of a stage's forward (embedding or received rows):
+// per-128-column sums of squares of x [d/128][npad] and z = x*g as the bf16
+// hi/lo B operand [2*npad][d] (RMSNorm applied by linearity in the GEMM).
+__global__ void norm_prep_kernel(const float* __restrict__ x, const bf16* __restrict__ g, bf16* z,
+                                 float* ssq, int d, const TickRows* rows) {
+  const int m = blockIdx.x, np = gridDim.x;
+  const bool live = m < rows->n_rows;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    const float v = live ? x[(size_t)m * d + k] * __bfloat162float(g[k]) : 0.f;
+    const bf16 hi = __float2bfloat16_rn(v);
+    z[(size_t)m * d + k] = hi;
+    z[(size_t)(np + m) * d + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
+  }
+  for (int t = threadIdx.x; t < d / 128; t += blockDim.x) {
+    float s = 0.f;
+    if (live)
+      for (int k = 0; k < 128; k++) {
+        const float v = x[(size_t)m * d + t * 128 + k];
+        s += v * v;
+      }
+    ssq[(size_t)t * np + m] = s;
+  }
+}
+
 // ---------------------------------------------------------------- RMSNorm
 // y = round(x * 1/sqrt(mean(x^2) + eps) * g)  (LLaMA RMSNorm; R18 rounding)
 // Rows >= n_rows are zero-filled (they are the padding columns of the GEMM).

@@ -66,6 +66,17 @@ struct GemmEpi {
   // STORE
   float* out;
   int ldo;
+  // RMSNorm feeding this GEMM, applied by linearity: the B operand is the hi/lo
+  // pair of x*g and the accumulator row m is scaled by inv[m] = 1/sqrt(ss/K+eps),
+  // ss summed from the producer's per-128-column partials (QKV / gate-up / head)
+  const float* scale_ssq;   // [scale_n][npad] or null
+  int scale_n;
+  float eps;
+  // RESID: per-tile sums of squares of the updated residual, and the next
+  // norm's B operand z = x_new * g_next as a bf16 hi/lo pair [2*npad][d]
+  float* ssq_out;           // [n_tiles][npad] or null
+  const bf16* z_gain;       // g of the next RMSNorm, or null
+  bf16* z_out;
 };
 
 // The activation operand carries each fp32 value as two bf16 rows (hi, lo:
@@ -81,13 +92,15 @@ struct GemmCfg {
   // NT=16: 5 stages -> ~110 KB, two CTAs per SM (the next GEMM's CTA starts
   // streaming its weights while this one drains: early PDL trigger)
   static constexpr int STAGES = NT <= 16 ? 5 : (NT <= 32 ? 4 : 3);
-  static constexpr int MIN_CTAS = NT <= 16 ? 2 : 1;
+  static constexpr int MIN_CTAS = NT <= 16 ? 2 : 1;   // ~110 KB: two CTAs per SM
   // two accumulator buffers (segment s uses buffer s&1) so the MMA of the next
   // tile segment never waits for the epilogue of the previous one
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int XCH_BYTES = 128 * (NT + 1) * 4;
   static constexpr int TOP_BYTES = 4 * NT * (int)sizeof(Top2);
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + XCH_BYTES + TOP_BYTES;
+  static constexpr int INV_BYTES = 64 * 4;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + XCH_BYTES + TOP_BYTES + INV_BYTES;
+  static constexpr int THREADS = 192;   // TMA producer, MMA issuer, 4 epilogue warps
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -151,8 +164,39 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     }
     named_bar_sync(1, 128);
   } else if (ep.mode == EPI_RESID) {
-    if (ng < sh.n_out)
-      for (int m = 0; m < n_rows && m < NT; m++) ep.x[(size_t)m * ep.d + ng] += v[m];
+    float sq[NT];
+#pragma unroll
+    for (int m = 0; m < NT; m++) {
+      sq[m] = 0.f;
+      if (m < n_rows && ng < sh.n_out) {
+        const float xn = ep.x[(size_t)m * ep.d + ng] + v[m];
+        ep.x[(size_t)m * ep.d + ng] = xn;
+        sq[m] = xn * xn;
+      }
+    }
+    if (ep.z_out && ng < sh.n_out) {  // next norm's B operand: x_new * g as a bf16 hi/lo pair
+      const float gv = __bfloat162float(ep.z_gain[ng]);
+      for (int m = 0; m < NT; m++) {
+        const float zv = (m < n_rows) ? ep.x[(size_t)m * ep.d + ng] * gv : 0.f;
+        const bf16 hi = __float2bfloat16_rn(zv);
+        ep.z_out[(size_t)m * ep.d + ng] = hi;
+        ep.z_out[(size_t)(NT + m) * ep.d + ng] = __float2bfloat16_rn(zv - __bfloat162float(hi));
+      }
+    }
+    if (ep.ssq_out) {  // deterministic per-tile sum of squares of the new residual rows
+#pragma unroll
+      for (int m = 0; m < NT; m++) {
+        float z = sq[m];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+        if (lane == 0) xch[q * NT + m] = z;
+      }
+      named_bar_sync(1, 128);
+      if (row < NT)
+        ep.ssq_out[(size_t)t * NT + row] =
+            ((xch[0 * NT + row] + xch[1 * NT + row]) + xch[2 * NT + row]) + xch[3 * NT + row];
+      named_bar_sync(1, 128);
+    }
   } else if (ep.mode == EPI_HEAD) {
     const bool valid = ng < ep.vocab;
     if (ep.logits && valid)
@@ -180,7 +224,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 }
 
 template <int NT>
-__global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
+__global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    GemmShape sh, GemmEpi ep) {
   using C = GemmCfg<NT>;
@@ -196,6 +240,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   int* s_flag = reinterpret_cast<int*>(tmem_holder + 1);
   float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   Top2* stop = reinterpret_cast<Top2*>(reinterpret_cast<uint8_t*>(xch) + C::XCH_BYTES);
+  float* s_inv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(stop) + C::TOP_BYTES);
 
   const int warp = warp_id(), lane = lane_id();
   const int G = gridDim.x, c = blockIdx.x;
@@ -235,13 +280,14 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
       int stage = 0;
       uint32_t phase = 0;
       const int pre = min(u1 - u0, C::STAGES);
+      const uint32_t tx = C::STAGE_BYTES;
       for (int i = 0; i < pre; i++) {
         const int u = u0 + i;
-        mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+        mbar_arrive_expect_tx(&full[i], tx);
         tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (u % KB) * 64, (u / KB) * 128, polA);
       }
       GEMM_PROBE(1);
-      pdl_wait();  // activations (B) are produced by the previous kernel
+      pdl_wait();  // activations / residual are produced by the previous kernel
       GEMM_PROBE(2);
       for (int i = 0; i < pre; i++) {
         const int u = u0 + i;
@@ -251,7 +297,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
       phase = (pre == C::STAGES) ? 1 : 0;
       for (int u = u0 + pre; u < u1; u++) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        mbar_arrive_expect_tx(&full[stage], tx);
         tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], (u % KB) * 64, (u / KB) * 128, polA);
         tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], (u % KB) * 64, 0, polB);
         if (++stage == C::STAGES) {
@@ -301,6 +347,16 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    if (ep.scale_ssq) {
+      // inv[m] of the RMSNorm applied by linearity (rows >= n_rows: padding)
+      pdl_wait();
+      if (row < NT) {
+        float ss = 0.f;
+        for (int i = 0; i < ep.scale_n; i++) ss += ep.scale_ssq[(size_t)i * NT + row];
+        s_inv[row] = 1.0f / sqrtf(ss / (float)sh.K + ep.eps);
+      }
+      named_bar_sync(1, 128);
+    }
     int seg = 0, u = u0;
     while (u < u1) {
       const int t = u / KB;
@@ -355,7 +411,13 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
         }
         named_bar_sync(1, 128);
       }
-      if (run_epi) gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop);
+      if (run_epi) {
+        if (ep.scale_ssq) {
+#pragma unroll
+          for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+        }
+        gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop);
+      }
       u = seg_end;
       seg++;
     }

@@ -16,3 +16,5 @@ for k in range(8):
     for it in (1, 50):
         us, by = gp.bench_kernel(k, it)
     print(f"{names[k]:12s} {us:9.2f} us  {by/1e6:8.2f} MB  {by/us/1e3 if us else 0:8.1f} GB/s")
+us, _ = gp.bench_kernel(8, 1)
+print("timeline stage span us", us)
