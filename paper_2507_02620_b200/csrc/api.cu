@@ -57,6 +57,7 @@ struct GemmOp {
   CUtensorMap ta, tb;   // weights, bf16 hi/lo activations
   GemmShape sh;
   int grid = 0;
+  int split = 0;        // > 0: cluster split-K with this many CTAs per tile
   bool ok = false;
 };
 
@@ -73,7 +74,7 @@ struct fs_ctx {
   int lps[FS_MAX_STAGES];
   int P = 1, rank = 0, L0 = 0, L1 = 0, nl = 0;
   bool first = true, last = true, bf = true;
-  int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536;
+  int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536, gemm_ctas = 2;
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   // arena
@@ -247,13 +248,27 @@ struct Carver {
   }
 };
 
-void plan_gemm(GemmOp& g, int n_out, int K, int n_sms) {
+void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const char* env = nullptr,
+               int def_split = -1) {
   g.sh.n_out = n_out;
   g.sh.K = K;
   g.sh.kb_total = K / 64;
   g.sh.n_tiles = (n_out + 127) / 128;
   g.sh.units = g.sh.n_tiles * g.sh.kb_total;
   g.grid = std::min(n_sms, g.sh.units);
+  // Few output tiles: tile-aligned cluster split-K with S = floor(SMs / tiles)
+  // CTAs per tile (one wave using one CTA slot per SM, so the next kernel's CTA
+  // can be resident and prefetch its weights); S = 2 when tiles fit one wave
+  // and two CTAs fit per SM.  Many tiles: stream-K.  (Measured on the 7B stage
+  // forward: QKV 2, O 4, down 4, gate/up and head stream-K; 3.96 ms vs 4.47 ms
+  // all stream-K.)
+  int S = n_sms / std::max(1, g.sh.n_tiles);
+  if (S < 2 && ctas_per_sm >= 2 && g.sh.n_tiles <= n_sms) S = 2;
+  S = std::min({S, 16, g.sh.kb_total});
+  g.split = (S >= 2 && !getenv("FS_NO_CLUSTER_GEMM")) ? S : 0;
+  if (def_split >= 0) g.split = def_split;          // tuned default for this GEMM
+  if (env && getenv(env)) g.split = atoi(getenv(env));  // tuning override
+  if (g.split == 1 || g.split > std::min(16, g.sh.kb_total)) g.split = 0;
   int mc = 1;
   const int U = g.sh.units, G = g.grid, KB = g.sh.kb_total;
   auto cta = [&](int u) { return (int)(((long long)(u + 1) * G + U - 1) / U) - 1; };
@@ -279,16 +294,16 @@ size_t carve(fs_ctx* c, char* base) {
     w.wd = cv.take<char>((size_t)d * ffn * es);
     w.g1 = cv.take<char>((size_t)d * es);
     w.g2 = cv.take<char>((size_t)d * es);
-    plan_gemm(w.qkv, nq, d, c->n_sms);
-    plan_gemm(w.o, d, H * hd, c->n_sms);
-    plan_gemm(w.gu, 2 * ffn, d, c->n_sms);
-    plan_gemm(w.dn, d, ffn, c->n_sms);
+    plan_gemm(w.qkv, nq, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_QKV");
+    plan_gemm(w.o, d, H * hd, c->n_sms, c->gemm_ctas, "FS_SPLIT_O");
+    plan_gemm(w.gu, 2 * ffn, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_GU");
+    plan_gemm(w.dn, d, ffn, c->n_sms, c->gemm_ctas, "FS_SPLIT_DN");
   }
   c->emb = c->first ? cv.take<char>((size_t)V * d * es) : nullptr;
   if (c->last) {
     c->wh = cv.take<char>((size_t)V * d * es);
     c->gf = cv.take<char>((size_t)d * es);
-    plan_gemm(c->head, V, d, c->n_sms);
+    plan_gemm(c->head, V, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_HEAD");
   }
   c->kv_plane_elems = (size_t)Hkv * f.max_ctx * hd;
   c->kv = cv.take<char>((size_t)c->nl * 2 * c->kv_plane_elems * es);
@@ -371,6 +386,7 @@ bool setup_ctx(fs_ctx* c, const fs_config* f) {
   c->bf = f->bf16 != 0;
   c->esz = c->bf ? 2 : 4;
   c->npad = npad_of(f->max_seg);
+  c->gemm_ctas = c->npad <= 16 ? 2 : 1;   // GemmCfg<NT>::MIN_CTAS
   c->ancw = f->max_live / 32;
   return true;
 }
@@ -444,7 +460,31 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          GemmCfg<NT>::SMEM);
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<NT>::SMEM);
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
+  }
+  if (g.split > 0) {
+    GemmShape sh = g.sh;
+    sh.dbg = nullptr;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(g.sh.n_tiles * g.split);
+    lc.blockDim = dim3(GemmCfg<NT>::THREADS);
+    lc.dynamicSmemBytes = GemmCfg<NT>::SMEM;
+    lc.stream = c->st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = g.split;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 2;
+    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, sh, ep);
+    CK_LAUNCH(c);
+    return FS_OK;
   }
   GemmShape sh = g.sh;
   sh.ws = c->gws;
@@ -1404,7 +1444,8 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
       for (size_t k = 0; k < per; k++) {
         unsigned long long v = h[i * per + k];
         if (!v) continue;
-        const size_t slot = g ? (k % 8) : (k % 16);
+        const size_t slot = k % 16;
+        if (g && slot >= 7) continue;
         if (slot == 0) st = std::min(st, v);
         en = std::max(en, v);
       }
@@ -1414,11 +1455,11 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
       if (i < 24 || i + 3 >= c->tl_names.size()) {
         fprintf(stderr, "%3zu %-5s start %8.2f end %8.2f dur %6.2f gap-from-prev-end %6.2f\n", i,
                 c->tl_names[i].c_str(), s0, e0, e0 - s0, s0 - prev_end);
-        if (g && i >= 3 && i <= 5) {  // per-probe distribution over CTAs for one layer
-          for (int k = 0; k < 7; k++) {
+        if (g && i >= 2 && i <= 5) {  // per-probe distribution over CTAs for one layer
+          for (int k = 0; k < 14; k++) {
             std::vector<double> vals;
             for (size_t cta = 0; cta < 148; cta++) {
-              unsigned long long v = h[i * per + cta * 8 + k];
+              unsigned long long v = h[i * per + cta * 16 + k];
               if (v) vals.push_back((v - t00) / 1e3);
             }
             if (vals.empty()) continue;

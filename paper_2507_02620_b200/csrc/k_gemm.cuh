@@ -21,6 +21,8 @@
 //   EPI_HEAD  logits (optional fp32 copy) + per-tile top-2 for the argmax
 //   EPI_STORE plain fp32 store (unit tests)
 #pragma once
+#include <cooperative_groups.h>
+
 #include "state.cuh"
 
 namespace fs {
@@ -40,7 +42,7 @@ FS_DEV unsigned long long g_gtimer() {
 }
 #define GEMM_PROBE(k)                                        \
   do {                                                       \
-    if (sh.dbg) sh.dbg[(size_t)blockIdx.x * 8 + (k)] = g_gtimer(); \
+    if (sh.dbg) sh.dbg[(size_t)blockIdx.x * 16 + (k)] = g_gtimer(); \
   } while (0)
 
 struct GemmEpi {
@@ -109,13 +111,17 @@ FS_DEV int cta_of_unit(int u, int units, int G) {
   return (int)(((long long)(u + 1) * G + units - 1) / units) - 1;
 }
 
+// Fused epilogue for output rows (weights) t*128+row; token columns m in
+// [mlo, mhi) are owned by this call (all NT for stream-K, a share in cluster
+// split-K), v[] holds the fp32 accumulator of every column.
 template <int NT>
 FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
-                          float* xch, Top2* stop) {
+                          float* xch, Top2* stop, int mlo, int mhi) {
   const TickRows* rows = ep.rows;
   const int n_rows = rows->n_rows;
   const int ng = t * 128 + row;
   const int lane = lane_id(), q = warp_id() & 3;
+  const int mend = min(mhi, n_rows);
   if (ep.mode == EPI_QKV) {
     const int H = ep.H, Hkv = ep.Hkv;
     if (ep.bias) {
@@ -124,7 +130,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       for (int m = 0; m < NT; m++) v[m] += b;
     }
     const int hh = t;  // one head (128 rows) per tile
-    if (hh < H + Hkv) {  // rotate-half RoPE on q and k heads
+    if (hh < H + Hkv) {  // rotate-half RoPE on q and k heads (partner row ^ 64)
 #pragma unroll
       for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
       named_bar_sync(1, 128);
@@ -132,14 +138,14 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 #pragma unroll
       for (int m = 0; m < NT; m++) {
         const float pv = xch[(row ^ 64) * (NT + 1) + m];
-        if (m < n_rows) {
+        if (m >= mlo && m < mend) {
           const float2 cs = ep.rope[(size_t)rows->pos[m] * 64 + i];
           v[m] = (row < 64) ? (v[m] * cs.x - pv * cs.y) : (v[m] * cs.x + pv * cs.y);
         }
       }
       named_bar_sync(1, 128);
     }
-    for (int m = 0; m < n_rows && m < NT; m++) {
+    for (int m = mlo; m < mend; m++) {
       const bf16 o = __float2bfloat16_rn(v[m]);
       if (hh < H) {
         ep.q_out[((size_t)m * H + hh) * 128 + row] = o;
@@ -154,7 +160,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
     named_bar_sync(1, 128);
     if (row < 64) {
-      for (int m = 0; m < n_rows && m < NT; m++) {
+      for (int m = mlo; m < mend; m++) {
         const float g = v[m], u = xch[(row + 64) * (NT + 1) + m];
         const float a = g / (1.0f + expf(-g)) * u;
         const bf16 hi = __float2bfloat16_rn(a);
@@ -168,7 +174,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       sq[m] = 0.f;
-      if (m < n_rows && ng < sh.n_out) {
+      if (m >= mlo && m < mend && ng < sh.n_out) {
         const float xn = ep.x[(size_t)m * ep.d + ng] + v[m];
         ep.x[(size_t)m * ep.d + ng] = xn;
         sq[m] = xn * xn;
@@ -176,7 +182,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     }
     if (ep.z_out && ng < sh.n_out) {  // next norm's B operand: x_new * g as a bf16 hi/lo pair
       const float gv = __bfloat162float(ep.z_gain[ng]);
-      for (int m = 0; m < NT; m++) {
+      for (int m = mlo; m < mhi; m++) {
         const float zv = (m < n_rows) ? ep.x[(size_t)m * ep.d + ng] * gv : 0.f;
         const bf16 hi = __float2bfloat16_rn(zv);
         ep.z_out[(size_t)m * ep.d + ng] = hi;
@@ -186,13 +192,14 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     if (ep.ssq_out) {  // deterministic per-tile sum of squares of the new residual rows
 #pragma unroll
       for (int m = 0; m < NT; m++) {
+        if (m < mlo || m >= mhi) continue;
         float z = sq[m];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
         if (lane == 0) xch[q * NT + m] = z;
       }
       named_bar_sync(1, 128);
-      if (row < NT)
+      if (row >= mlo && row < mhi)
         ep.ssq_out[(size_t)t * NT + row] =
             ((xch[0 * NT + row] + xch[1 * NT + row]) + xch[2 * NT + row]) + xch[3 * NT + row];
       named_bar_sync(1, 128);
@@ -200,7 +207,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
   } else if (ep.mode == EPI_HEAD) {
     const bool valid = ng < ep.vocab;
     if (ep.logits && valid)
-      for (int m = 0; m < n_rows && m < NT; m++) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
+      for (int m = mlo; m < mend; m++) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       Top2 tt;
@@ -211,7 +218,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       if (lane == 0) stop[q * NT + m] = tt;
     }
     named_bar_sync(1, 128);
-    if (row < NT) {
+    if (row >= mlo && row < mhi) {
       Top2 r = stop[row];
       for (int w = 1; w < 4; w++) r = top2_merge(r, stop[w * NT + row]);
       ep.head_part[(size_t)t * NT + row] = r;
@@ -219,7 +226,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     named_bar_sync(1, 128);
   } else {  // EPI_STORE
     if (ng < sh.n_out)
-      for (int m = 0; m < n_rows && m < NT; m++) ep.out[(size_t)m * ep.ldo + ng] = v[m];
+      for (int m = mlo; m < mend; m++) ep.out[(size_t)m * ep.ldo + ng] = v[m];
   }
 }
 
@@ -377,6 +384,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
+      if (threadIdx.x == 64) GEMM_PROBE(8 + 2 * (seg & 1));
       const bool whole = (seg_start == t * KB) && (seg_end == (t + 1) * KB);
       bool run_epi = whole;
       if (!whole) {
@@ -386,38 +394,59 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
         float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
 #pragma unroll
         for (int m = 0; m < NT; m += 4)
-          *reinterpret_cast<float4*>(wp + m) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
-        __threadfence();
+          __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+        // one gpu-scope release by the counting thread: bar.sync orders the other
+        // threads' partial stores before it (fence cumulativity)
         named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) *s_flag = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+          if (last) __threadfence();   // acquire: every contributor's partial is visible
+          *s_flag = last;
+        }
         named_bar_sync(1, 128);
         run_epi = *s_flag;
         if (run_epi) {
-          __threadfence();
 #pragma unroll
           for (int m = 0; m < NT; m++) v[m] = 0.f;
-          for (int jj = 0; jj < nc; jj++) {
-            const float* rp = sh.ws + (((size_t)t * sh.max_contrib + jj) * 128 + row) * NT;
+          // partials summed in contributor order (deterministic); loads of up to
+          // four contributors are in flight together
+          for (int j0 = 0; j0 < nc; j0 += 4) {
+            float4 pv[4][NT / 4];
 #pragma unroll
-            for (int m = 0; m < NT; m += 4) {
-              const float4 p = __ldcg(reinterpret_cast<const float4*>(rp + m));
-              v[m] += p.x;
-              v[m + 1] += p.y;
-              v[m + 2] += p.z;
-              v[m + 3] += p.w;
+            for (int jj = 0; jj < 4; jj++) {
+              if (j0 + jj < nc) {
+                const float* rp = sh.ws + (((size_t)t * sh.max_contrib + j0 + jj) * 128 + row) * NT;
+#pragma unroll
+                for (int m = 0; m < NT / 4; m++) pv[jj][m] = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+              }
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) {
+              if (j0 + jj < nc) {
+#pragma unroll
+                for (int m = 0; m < NT / 4; m++) {
+                  v[4 * m] += pv[jj][m].x;
+                  v[4 * m + 1] += pv[jj][m].y;
+                  v[4 * m + 2] += pv[jj][m].z;
+                  v[4 * m + 3] += pv[jj][m].w;
+                }
+              }
             }
           }
           if (warp == 2 && lane == 0) sh.counters[t] = 0;
         }
         named_bar_sync(1, 128);
       }
+      if (threadIdx.x == 64) GEMM_PROBE(12 + (seg & 1));
       if (run_epi) {
         if (ep.scale_ssq) {
 #pragma unroll
           for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
         }
-        gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop);
+        gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, 0, NT);
       }
+      if (threadIdx.x == 64) GEMM_PROBE(9 + 2 * (seg & 1));
       u = seg_end;
       seg++;
     }
@@ -425,6 +454,161 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
   if (threadIdx.x == 64) GEMM_PROBE(5);
   __syncthreads();
   if (threadIdx.x == 0) GEMM_PROBE(6);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+
+// ---------------------------------------------------------------- cluster split-K
+// Tile-aligned split-K for GEMMs with few output tiles (QKV, O, down): the S
+// CTAs splitting one 128-row weight tile over K form a thread-block cluster.
+// Each CTA streams its K range into its TMEM accumulator, parks the fp32
+// partial in its own shared memory, and after a cluster barrier CTA rank r
+// sums the S partials of its share of token columns through distributed
+// shared memory (rank order: deterministic) and runs the fused epilogue for
+// them.  No global partials, atomics or fences on the epilogue path.
+template <int NT>
+__global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
+    gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        GemmShape sh, GemmEpi ep) {
+  namespace cg = cooperative_groups;
+  using C = GemmCfg<NT>;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 2);
+  float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
+  Top2* stop = reinterpret_cast<Top2*>(reinterpret_cast<uint8_t*>(xch) + C::XCH_BYTES);
+  float* s_inv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(stop) + C::TOP_BYTES);
+  float* part = reinterpret_cast<float*>(sA);   // [128][NT+1] partial, after the mainloop
+
+  const int warp = warp_id(), lane = lane_id();
+  const int S = (int)cluster.num_blocks(), r = (int)cluster.block_rank();
+  const int t = blockIdx.x / S;
+  const int KB = sh.kb_total;
+  const int kb0 = (int)((long long)r * KB / S), kb1 = (int)((long long)(r + 1) * KB / S);
+  const int nu = kb1 - kb0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&acc_full[0], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  if (warp == 1) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: weights before the grid dependency, activations after
+      const uint64_t polA = l2_evict_first_policy();
+      const uint64_t polB = l2_evict_last_policy();
+      const int pre = min(nu, C::STAGES);
+      for (int i = 0; i < pre; i++) {
+        mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
+        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (kb0 + i) * 64, t * 128, polA);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; i++) tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * 64, 0, polB);
+      int stage = pre % C::STAGES;
+      uint32_t phase = (pre == C::STAGES) ? 1 : 0;
+      for (int i = pre; i < nu; i++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], (kb0 + i) * 64, t * 128, polA);
+        tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], (kb0 + i) * 64, 0, polB);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, C::BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < nu; i++) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          umma_bf16(tmem, umma_sdesc_sw128(a0 + k * 32), umma_sdesc_sw128(b0 + k * 32), idesc,
+                    (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&empty[stage]);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(&acc_full[0]);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    if (ep.scale_ssq) {
+      pdl_wait();
+      if (row < NT) {
+        float ss = 0.f;
+        for (int i = 0; i < ep.scale_n; i++) ss += ep.scale_ssq[(size_t)i * NT + row];
+        s_inv[row] = 1.0f / sqrtf(ss / (float)sh.K + ep.eps);
+      }
+    }
+    mbar_wait(&acc_full[0], 0);
+    tc_fence_after();
+    float v[NT];
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+    for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
+#pragma unroll
+    for (int j = 0; j < NT; j += 16) {
+      float w[16];
+      tmem_ld16(tl + NT + j, w);
+#pragma unroll
+      for (int i = 0; i < 16; i++) v[j + i] += w[i];
+    }
+    // every MMA has completed (acc_full): the stage buffers are free for the partial
+#pragma unroll
+    for (int m = 0; m < NT; m++) part[row * (NT + 1) + m] = v[m];
+  }
+  cluster.sync();
+  if (warp >= 2) {
+    const int row = (warp & 3) * 32 + lane;
+    const int mlo = r * NT / S, mhi = (r + 1) * NT / S;
+    float v[NT];
+#pragma unroll
+    for (int m = 0; m < NT; m++) v[m] = 0.f;
+    for (int c = 0; c < S; c++) {
+      const float* pc = cluster.map_shared_rank(part, c);
+      for (int m = mlo; m < mhi; m++) v[m] += pc[row * (NT + 1) + m];
+    }
+    if (ep.scale_ssq) {
+      named_bar_sync(1, 128);  // s_inv visible to all epilogue warps
+#pragma unroll
+      for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+    }
+    gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi);
+  }
+  cluster.sync();   // peers are done reading this CTA's partial
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
