@@ -255,6 +255,7 @@ void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const ch
   g.sh.kb_total = K / 64;
   g.sh.n_tiles = (n_out + 127) / 128;
   g.sh.units = g.sh.n_tiles * g.sh.kb_total;
+  g.sh.late_trigger = getenv("FS_LATE_TRIGGER") ? 1 : 0;
   g.grid = std::min(n_sms, g.sh.units);
   // Few output tiles: tile-aligned cluster split-K with S = floor(SMs / tiles)
   // CTAs per tile (one wave using one CTA slot per SM, so the next kernel's CTA
@@ -468,6 +469,10 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   if (g.split > 0) {
     GemmShape sh = g.sh;
     sh.dbg = nullptr;
+    if (c->tl_buf) {
+      sh.dbg = c->tl_buf + c->tl_names.size() * 8192;
+      c->tl_names.push_back("gemm");
+    }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(g.sh.n_tiles * g.split);
     lc.blockDim = dim3(GemmCfg<NT>::THREADS);
@@ -491,7 +496,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   sh.counters = c->gcnt;
   sh.dbg = c->gemm_dbg;
   if (c->tl_buf) {
-    sh.dbg = c->tl_buf + c->tl_names.size() * 4096;
+    sh.dbg = c->tl_buf + c->tl_names.size() * 8192;
     c->tl_names.push_back("gemm");
   }
   cudaLaunchConfig_t lc = {};
@@ -583,7 +588,7 @@ int launch_attention(fs_ctx* c, int l) {
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
     a.dbg = c->att_dbg;
     if (c->tl_buf) {
-      a.dbg = c->tl_buf + c->tl_names.size() * 4096;
+      a.dbg = c->tl_buf + c->tl_names.size() * 8192;
       c->tl_names.push_back("attn");
     }
     const int G = H / Hkv, QR = G * np, MT = QR / 16;
@@ -1426,7 +1431,7 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
   if (kind == 8) {
     // timeline of one (non-graph) stage forward: per probed launch, first CTA start and last
     // CTA end relative to the first launch's start
-    const size_t per = 4096, nl = 400;
+    const size_t per = 8192, nl = 400;
     CK_CUDA(c, cudaMalloc(&c->tl_buf, per * nl * 8));
     cudaMemsetAsync(c->tl_buf, 0, per * nl * 8, c->st);
     c->tl_names.clear();
@@ -1455,10 +1460,11 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
       if (i < 24 || i + 3 >= c->tl_names.size()) {
         fprintf(stderr, "%3zu %-5s start %8.2f end %8.2f dur %6.2f gap-from-prev-end %6.2f\n", i,
                 c->tl_names[i].c_str(), s0, e0, e0 - s0, s0 - prev_end);
-        if (g && i >= 2 && i <= 5) {  // per-probe distribution over CTAs for one layer
+        if (g && i >= 7 && i <= 11) {  // per-probe distribution over CTAs for one layer
           for (int k = 0; k < 14; k++) {
+            if (k == 7 || (k >= 10)) continue;
             std::vector<double> vals;
-            for (size_t cta = 0; cta < 148; cta++) {
+            for (size_t cta = 0; cta < 512; cta++) {
               unsigned long long v = h[i * per + cta * 16 + k];
               if (v) vals.push_back((v - t00) / 1e3);
             }

@@ -682,11 +682,19 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     const int m = rr % a.npad, g = rr / a.npad;
     if (m >= n_rows) continue;
     const int q4 = (tid & 31) * 4;
-    float mm[8], M = -INFINITY;
+    float mm[8], ll[8], M = -INFINITY;
+    float4 oo[8];
 #pragma unroll
-    for (int c = 0; c < 8; c++) {
+    for (int c = 0; c < 8; c++) {   // all ranks' loads in flight together
       mm[c] = -INFINITY;
-      if (c < nsplit) mm[c] = cluster.map_shared_rank(sPml, c)[rr * 2];
+      ll[c] = 0.f;
+      oo[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < nsplit) {
+        const uint32_t pm = dsmem_addr(sPml + rr * 2, (uint32_t)c);
+        mm[c] = ld_dsmem_f32(pm);
+        ll[c] = ld_dsmem_f32(pm + 4);
+        oo[c] = ld_dsmem_f32x4(dsmem_addr(sPart + rr * ATT_HD + q4, (uint32_t)c));
+      }
       M = fmaxf(M, mm[c]);
     }
     float L = 0.f;
@@ -695,12 +703,11 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     for (int c = 0; c < 8; c++) {
       if (c < nsplit && mm[c] != -INFINITY) {
         const float wt = exp2f(mm[c] - M);
-        L += cluster.map_shared_rank(sPml, c)[rr * 2 + 1] * wt;
-        const float4 o = *reinterpret_cast<const float4*>(cluster.map_shared_rank(sPart, c) + rr * ATT_HD + q4);
-        acc.x += o.x * wt;
-        acc.y += o.y * wt;
-        acc.z += o.z * wt;
-        acc.w += o.w * wt;
+        L += ll[c] * wt;
+        acc.x += oo[c].x * wt;
+        acc.y += oo[c].y * wt;
+        acc.z += oo[c].z * wt;
+        acc.w += oo[c].w * wt;
       }
     }
     const float v[4] = {acc.x / L, acc.y / L, acc.z / L, acc.w / L};

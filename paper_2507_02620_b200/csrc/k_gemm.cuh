@@ -33,6 +33,7 @@ struct GemmShape {
   int n_out, K, kb_total, n_tiles, units, max_contrib;
   float* ws;       // [n_tiles][max_contrib][128][NT] fp32 partials
   int* counters;   // [n_tiles], zero between launches
+  int late_trigger; // diagnostics: trigger dependents at exit instead of at start
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (diagnostics)
 };
 FS_DEV unsigned long long g_gtimer() {
@@ -116,7 +117,7 @@ FS_DEV int cta_of_unit(int u, int units, int G) {
 // split-K), v[] holds the fp32 accumulator of every column.
 template <int NT>
 FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
-                          float* xch, Top2* stop, int mlo, int mhi) {
+                          float* xch, Top2* stop, int mlo, int mhi, const float* xpre = nullptr) {
   const TickRows* rows = ep.rows;
   const int n_rows = rows->n_rows;
   const int ng = t * 128 + row;
@@ -145,7 +146,9 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       }
       named_bar_sync(1, 128);
     }
-    for (int m = mlo; m < mend; m++) {
+#pragma unroll
+    for (int m = 0; m < NT; m++) {
+      if (m < mlo || m >= mend) continue;
       const bf16 o = __float2bfloat16_rn(v[m]);
       if (hh < H) {
         ep.q_out[((size_t)m * H + hh) * 128 + row] = o;
@@ -160,7 +163,9 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
     named_bar_sync(1, 128);
     if (row < 64) {
-      for (int m = mlo; m < mend; m++) {
+#pragma unroll
+      for (int m = 0; m < NT; m++) {
+        if (m < mlo || m >= mend) continue;
         const float g = v[m], u = xch[(row + 64) * (NT + 1) + m];
         const float a = g / (1.0f + expf(-g)) * u;
         const bf16 hi = __float2bfloat16_rn(a);
@@ -170,20 +175,28 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     }
     named_bar_sync(1, 128);
   } else if (ep.mode == EPI_RESID) {
-    float sq[NT];
+    float sq[NT], xn[NT];
+    // old residual values first (all loads in flight), then the update
+#pragma unroll
+    for (int m = 0; m < NT; m++) {
+      xn[m] = 0.f;
+      if (m >= mlo && m < mend && ng < sh.n_out) xn[m] = xpre ? xpre[m] : ep.x[(size_t)m * ep.d + ng];
+    }
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       sq[m] = 0.f;
       if (m >= mlo && m < mend && ng < sh.n_out) {
-        const float xn = ep.x[(size_t)m * ep.d + ng] + v[m];
-        ep.x[(size_t)m * ep.d + ng] = xn;
-        sq[m] = xn * xn;
+        xn[m] += v[m];
+        ep.x[(size_t)m * ep.d + ng] = xn[m];
+        sq[m] = xn[m] * xn[m];
       }
     }
     if (ep.z_out && ng < sh.n_out) {  // next norm's B operand: x_new * g as a bf16 hi/lo pair
       const float gv = __bfloat162float(ep.z_gain[ng]);
-      for (int m = mlo; m < mhi; m++) {
-        const float zv = (m < n_rows) ? ep.x[(size_t)m * ep.d + ng] * gv : 0.f;
+#pragma unroll
+      for (int m = 0; m < NT; m++) {
+        if (m < mlo || m >= mhi) continue;
+        const float zv = (m < n_rows) ? xn[m] * gv : 0.f;
         const bf16 hi = __float2bfloat16_rn(zv);
         ep.z_out[(size_t)m * ep.d + ng] = hi;
         ep.z_out[(size_t)(NT + m) * ep.d + ng] = __float2bfloat16_rn(zv - __bfloat162float(hi));
@@ -207,7 +220,9 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
   } else if (ep.mode == EPI_HEAD) {
     const bool valid = ng < ep.vocab;
     if (ep.logits && valid)
-      for (int m = mlo; m < mend; m++) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
+#pragma unroll
+      for (int m = 0; m < NT; m++)
+        if (m >= mlo && m < mend) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       Top2 tt;
@@ -226,7 +241,9 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     named_bar_sync(1, 128);
   } else {  // EPI_STORE
     if (ng < sh.n_out)
-      for (int m = mlo; m < mend; m++) ep.out[(size_t)m * ep.ldo + ng] = v[m];
+#pragma unroll
+      for (int m = 0; m < NT; m++)
+        if (m >= mlo && m < mend) ep.out[(size_t)m * ep.ldo + ng] = v[m];
   }
 }
 
@@ -276,7 +293,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
   const uint32_t tmem = *tmem_holder;
   // dependents may launch now: they prefetch their weights and wait on
   // griddepcontrol.wait (full completion of this grid) before reading outputs
-  pdl_trigger();
+  if (!sh.late_trigger) pdl_trigger();
 
   if (warp == 0) {
     // ---------------- TMA producer: weights never depend on the previous
@@ -487,7 +504,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   float* xch = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE_BYTES + 256);
   Top2* stop = reinterpret_cast<Top2*>(reinterpret_cast<uint8_t*>(xch) + C::XCH_BYTES);
   float* s_inv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(stop) + C::TOP_BYTES);
-  float* part = reinterpret_cast<float*>(sA);   // [128][NT+1] partial, after the mainloop
+  float* part = reinterpret_cast<float*>(sA);   // [NT][128] partial (column-major), after the mainloop
 
   const int warp = warp_id(), lane = lane_id();
   const int S = (int)cluster.num_blocks(), r = (int)cluster.block_rank();
@@ -495,6 +512,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   const int KB = sh.kb_total;
   const int kb0 = (int)((long long)r * KB / S), kb1 = (int)((long long)(r + 1) * KB / S);
   const int nu = kb1 - kb0;
+  if (threadIdx.x == 0) GEMM_PROBE(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -512,7 +530,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  pdl_trigger();
+  if (!sh.late_trigger) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: weights before the grid dependency, activations after
@@ -523,7 +541,9 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
         mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
         tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (kb0 + i) * 64, t * 128, polA);
       }
+      GEMM_PROBE(1);
       pdl_wait();
+      GEMM_PROBE(2);
       for (int i = 0; i < pre; i++) tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * 64, 0, polB);
       int stage = pre % C::STAGES;
       uint32_t phase = (pre == C::STAGES) ? 1 : 0;
@@ -546,6 +566,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
       uint32_t phase = 0;
       for (int i = 0; i < nu; i++) {
         mbar_wait(&full[stage], phase);
+        if (i == 0) GEMM_PROBE(3);
         tc_fence_after();
         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
         const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
@@ -560,6 +581,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
         }
       }
       umma_commit(&acc_full[0]);
+      GEMM_PROBE(4);
     }
     __syncwarp();
   } else {
@@ -588,27 +610,68 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     }
     // every MMA has completed (acc_full): the stage buffers are free for the partial
 #pragma unroll
-    for (int m = 0; m < NT; m++) part[row * (NT + 1) + m] = v[m];
+    for (int m = 0; m < NT; m++) part[m * 128 + row] = v[m];
+  }
+  // residual values of my token columns, loaded before the barrier (RESID)
+  float xpre[NT];
+  if (warp >= 2 && ep.mode == EPI_RESID) {
+    const int row = (warp & 3) * 32 + lane;
+    const int ng = t * 128 + row;
+    const int mlo = r * NT / S, mhi = min((r + 1) * NT / S, ep.rows->n_rows);
+#pragma unroll
+    for (int m = 0; m < NT; m++)
+      xpre[m] = (m >= mlo && m < mhi && ng < sh.n_out) ? ep.x[(size_t)m * ep.d + ng] : 0.f;
   }
   cluster.sync();
+  if (threadIdx.x == 64) GEMM_PROBE(8);
   if (warp >= 2) {
     const int row = (warp & 3) * 32 + lane;
     const int mlo = r * NT / S, mhi = (r + 1) * NT / S;
     float v[NT];
 #pragma unroll
     for (int m = 0; m < NT; m++) v[m] = 0.f;
-    for (int c = 0; c < S; c++) {
-      const float* pc = cluster.map_shared_rank(part, c);
-      for (int m = mlo; m < mhi; m++) v[m] += pc[row * (NT + 1) + m];
+    // DSMEM partials of every rank for my columns: issue up to 4 ranks' loads
+    // together, accumulate in rank order (deterministic)
+    constexpr int MW = (NT + 1) / 2;   // max columns per rank (S >= 2)
+    float acc[MW];
+#pragma unroll
+    for (int j = 0; j < MW; j++) acc[j] = 0.f;
+    for (int c0 = 0; c0 < S; c0 += 4) {
+      float pv[4][MW];
+#pragma unroll
+      for (int cc = 0; cc < 4; cc++) {
+        if (c0 + cc < S) {
+          const uint32_t pc = dsmem_addr(part + mlo * 128 + row, (uint32_t)(c0 + cc));
+#pragma unroll
+          for (int j = 0; j < MW; j++)
+            if (mlo + j < mhi) pv[cc][j] = ld_dsmem_f32(pc + j * 128 * 4);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; cc++) {
+        if (c0 + cc < S) {
+#pragma unroll
+          for (int j = 0; j < MW; j++) acc[j] += (mlo + j < mhi) ? pv[cc][j] : 0.f;
+        }
+      }
     }
+    if (threadIdx.x == 64) GEMM_PROBE(9);
+    // scatter acc[j] -> v[mlo + j] with static register indices
+#pragma unroll
+    for (int m = 0; m < NT; m++)
+#pragma unroll
+      for (int j = 0; j < MW; j++)
+        if (m == mlo + j && m < mhi) v[m] = acc[j];
     if (ep.scale_ssq) {
       named_bar_sync(1, 128);  // s_inv visible to all epilogue warps
 #pragma unroll
       for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
     }
-    gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi);
+    gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi, ep.mode == EPI_RESID ? xpre : nullptr);
   }
+  if (threadIdx.x == 64) GEMM_PROBE(5);
   cluster.sync();   // peers are done reading this CTA's partial
+  if (threadIdx.x == 0) GEMM_PROBE(6);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
