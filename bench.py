@@ -72,7 +72,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -101,7 +101,8 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ our arm
-def run_round(gp, tree, l_max):
+def run_round(gp, tree, l_max, tokens_out=None):
+    """One SD round: submit, ticks, accept, prune until the round exits."""
     from paper_2507_02620_b200 import flowspec as F
     gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], l_max)
     committed = 0
@@ -113,6 +114,8 @@ def run_round(gp, tree, l_max):
         if not d.progress:
             continue
         committed += d.n_acc
+        if tokens_out is not None:
+            tokens_out += list(d.acc_tokens[:d.n_acc])
         gp.fs_prune_and_compact(d)
         if not d.cont:
             return committed, ticks
@@ -133,6 +136,38 @@ def greedy_stream(gp, count):
                 out.append(d.x_new)
                 break
     return out
+
+
+def plan_schedule(gp, prefix, ranks, n_rounds, n_nodes, depth, l_max, shape, max_iter=6):
+    """Draft-provider stand-in: trees whose planted path is the model's greedy
+    continuation.  The plan starts as an AR greedy stream; each untimed dry run
+    of all rounds replaces it with the stream tree verification actually
+    commits (a flagged near-tie can make it differ from the AR stream) plus an
+    AR continuation, until a dry run follows its plan.  The timed rounds then
+    replay exactly these trees from the same prefix (deterministic)."""
+    from paper_2507_02620_b200 import flowspec as F
+    from synth import gen
+    a = len(ranks) - 1
+    need = n_rounds * (a + 1) + a + 2
+    plan = greedy_stream(gp, need)
+    trees, diverged = [], 0
+    for it in range(max_iter):
+        gp.fs_set_prefix(prefix, F.FS_PREFILL)
+        trees, committed, diverged = [], [], 0
+        for r in range(n_rounds):
+            c = len(committed)
+            root = gp.state()["x_new"]
+            if c + a + 2 <= len(plan) and plan[c] == root:
+                t = gen.planted_tree(SEED + r, n_nodes, depth, plan[c:c + a + 2], ranks, shape.vocab)
+            else:  # off plan: unplanted tree rooted at the actual next token
+                diverged += 1
+                t = gen.random_tree(SEED + 7 * r, n_nodes, depth, shape.vocab, root)
+            trees.append(t)
+            run_round(gp, t, l_max, committed)
+        if diverged == 0 and committed == plan[:len(committed)]:
+            return trees, 0, it + 1
+        plan = committed + greedy_stream(gp, need)
+    return trees, diverged, max_iter
 
 
 def ours(args):
@@ -165,31 +200,23 @@ def ours(args):
                     device=local, nccl_id=nccl_id)
     gp.fs_load_random_weights(SEED)
     prefix = gen.prefix_tokens(SEED, args.prefix, shape.vocab)
-    x0 = gp.fs_set_prefix(prefix, F.FS_PREFILL)
+    gp.fs_set_prefix(prefix, F.FS_PREFILL)
     n_rounds = W + 2 * K
-    stream = greedy_stream(gp, n_rounds * (a + 1) + a + 2)
-    assert gp.fs_set_prefix(prefix, F.FS_PREFILL) == x0 == stream[0]
-    trees = [gen.planted_tree(SEED + r, n_nodes, depth, stream[r * (a + 1): r * (a + 1) + a + 2],
-                              ranks, shape.vocab) for r in range(n_rounds)]
-    diverged = 0
+    trees, diverged, dry_runs = plan_schedule(gp, prefix, ranks, n_rounds, n_nodes, depth, l_max, shape)
+    gp.fs_set_prefix(prefix, F.FS_PREFILL)
 
     def round_r(r):
-        nonlocal diverged
-        t = trees[r]
-        if gp.state()["x_new"] != int(t["token"][0]):   # planted path lost (near-tie)
-            diverged += 1
-            t = gen.random_tree(SEED + 7 * r, n_nodes, depth, shape.vocab, gp.state()["x_new"])
-        return run_round(gp, t, l_max)
+        return run_round(gp, trees[r], l_max)
 
-    for r in range(W):
-        round_r(r)
     st = gp.stream
     clocks = Clocks(local)
+    clocks.start()
+    for r in range(W):
+        round_r(r)
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = gp.state()["launches"]
-    clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     tokens = ticks = 0
@@ -201,7 +228,6 @@ def ours(args):
     torch.cuda.synchronize()
     if P > 1:
         dist.barrier()
-    clk = clocks.stop()
     launches = gp.state()["launches"] - launches0
     dev_ms = e0.elapsed_time(e1)
     if P > 1:
@@ -226,6 +252,7 @@ def ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
     e2e = e_tokens / wall
+    clk = clocks.stop()
 
     # roofline of the dominant kernel (weight-streaming GEMM): CUDA-event pairs
     # around every GEMM / attention launch over K profiled rounds
@@ -275,6 +302,7 @@ def ours(args):
             "tokens_per_step": tokens / K,
             "ticks_per_step": ticks / K,
             "planted_path_divergences": diverged,
+            "schedule_dry_runs": dry_runs,
         },
         "clocks": clk,
         "e2e": {"value": round(e2e, 3), "unit": "tok/s",

@@ -1460,6 +1460,20 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
       if (i < 24 || i + 3 >= c->tl_names.size()) {
         fprintf(stderr, "%3zu %-5s start %8.2f end %8.2f dur %6.2f gap-from-prev-end %6.2f\n", i,
                 c->tl_names[i].c_str(), s0, e0, e0 - s0, s0 - prev_end);
+        if (!g && i >= 6 && i <= 11) {  // attention phases over CTAs (one layer)
+          for (int k = 0; k < 15; k++) {
+            std::vector<double> vals;
+            for (size_t cta = 0; cta < 512; cta++) {
+              unsigned long long v = h[i * per + cta * 16 + k];
+              if (v) vals.push_back((v - t00) / 1e3);
+            }
+            if (vals.empty()) continue;
+            std::sort(vals.begin(), vals.end());
+            fprintf(stderr, "      aprobe %2d: min %8.2f p10 %8.2f med %8.2f p90 %8.2f max %8.2f (n=%zu)\n", k,
+                    vals[0], vals[vals.size() / 10], vals[vals.size() / 2], vals[vals.size() * 9 / 10],
+                    vals.back(), vals.size());
+          }
+        }
         if (g && i >= 7 && i <= 11) {  // per-probe distribution over CTAs for one layer
           for (int k = 0; k < 14; k++) {
             if (k == 7 || (k >= 10)) continue;

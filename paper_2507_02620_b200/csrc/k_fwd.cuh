@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   const int npre = min(nsc, ATT_NBUF);
   int issued = 0;
   while (issued < npre && kbeg + (issued + 1) * ATT_SUB <= first_written) load_sub(issued++);
+  const int n_early = issued;   // sub-chunk groups committed before the Q group
   pdl_wait();
   const int n_rows = rows->n_rows;
   // Q (GQA-packed rows) and the ancestor rows: one cp.async group
@@ -521,9 +522,13 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   // groups committed so far: pre-dependency sub-chunks, Q, remaining prefetch;
   // wait until sub-chunk sc and Q have landed
   for (int sc = 0; sc < nsc; sc++) {
-    const int pending_after = issued - 1 - sc;   // sub-chunk groups younger than sc
-    if (pending_after >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-    else if (pending_after == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    // cp.async groups in commit order: early sub-chunks, Q, later sub-chunks.
+    // Both sub-chunk sc and Q must have landed: allow only the groups younger
+    // than the younger of the two to stay pending.
+    const int need = (sc < n_early) ? n_early : sc + 1;   // group index
+    const int allowed = issued - need;                     // groups committed = issued + 1
+    if (allowed >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else if (allowed == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     ATT_PROBE(2 + sc);
