@@ -66,7 +66,9 @@ class Clocks:
     def __init__(self, index):
         self.index = index
         self.rows = []
+        self.times = []
         self.proc = None
+        self.t_from = 0.0
 
     def start(self):
         try:
@@ -84,6 +86,10 @@ class Clocks:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
                 self.rows.append(parts)
+                self.times.append(time.perf_counter())
+
+    def count_since(self, t0):
+        return sum(1 for t in self.times if t >= t0)
 
     def stop(self):
         if self.proc:
@@ -92,10 +98,11 @@ class Clocks:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        sm = sorted(int(r[0]) for r in self.rows if r[0].isdigit())
-        mx = max([int(r[1]) for r in self.rows if r[1].isdigit()] or [0])
+        rows = [r for r, t in zip(self.rows, self.times) if t >= self.t_from] or self.rows
+        sm = sorted(int(r[0]) for r in rows if r[0].isdigit())
+        mx = max([int(r[1]) for r in rows if r[1].isdigit()] or [0])
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None,
                 "reasons": reasons, "samples": len(sm)}
 
@@ -196,6 +203,8 @@ def ours(args):
     l_max, n_nodes, depth = 16, 64, 6
     W, K = args.warmup, args.steps
     max_ctx = args.prefix + (W + 2 * K + 4) * (a + 1) + 600
+    clocks = Clocks(local)   # nvidia-smi needs ~1 s to start sampling
+    clocks.start()
     gp = F.Pipeline(shape, n_stages=P, rank=rank, max_ctx=max_ctx, max_live=512, max_seg=16,
                     device=local, nccl_id=nccl_id)
     gp.fs_load_random_weights(SEED)
@@ -209,14 +218,13 @@ def ours(args):
         return run_round(gp, trees[r], l_max)
 
     st = gp.stream
-    clocks = Clocks(local)
-    clocks.start()
     for r in range(W):
         round_r(r)
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = gp.state()["launches"]
+    clocks.t_from = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     tokens = ticks = 0
@@ -252,6 +260,20 @@ def ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
     e2e = e_tokens / wall
+    # keep the same load (one-node verify rounds) until the sampler has seen
+    # a few samples since the timed region started
+    hold_t0 = time.perf_counter()
+    while True:
+        more = clocks.count_since(clocks.t_from) < 4 and time.perf_counter() - hold_t0 < 3.0
+        if P > 1:  # every rank must run the same number of collective ticks
+            flag = torch.tensor([1 if more else 0], device="cuda")
+            dist.broadcast(flag, src=0)
+            more = bool(flag.item())
+        if not more:
+            break
+        greedy_stream(gp, 4)
+    if P > 1:
+        dist.barrier()
     clk = clocks.stop()
 
     # roofline of the dominant kernel (weight-streaming GEMM): CUDA-event pairs
