@@ -93,3 +93,88 @@ def test_bf16_synth_prefix_and_kv_rows():
     st = run_lockstep(gp, op, planted_trees(shape, 40, 6, (0, 2, 5, 17, 21), SEED), n_rounds=2,
                       l_max=16, tol=2e-2)
     assert st.max_abs <= 2e-2
+
+
+def _append_batch(op, rng, n_new, vocab):
+    """Random APPEND batch (a16): parents are live nodes or earlier
+    batch nodes; sibling tokens unique; own scores in (0, 1]."""
+    live = list(op.node)
+    kids = {}
+    for s in range(len(op.node)):
+        if op.par[s] >= 0:
+            kids.setdefault(op.node[op.par[s]], set()).add(op.tok[s])
+    base = op.next_id
+    parent, token, own = [], [], []
+    for i in range(n_new):
+        cand = live + [base + j for j in range(i)]
+        p = cand[rng.below(len(cand))]
+        while True:
+            t = rng.below(vocab)
+            if t not in kids.setdefault(p, set()):
+                break
+        kids[p].add(t)
+        parent.append(p)
+        token.append(t)
+        own.append(np.float32(0.05 + 0.95 * rng.uniform()))
+    return parent, token, own
+
+
+@pytest.mark.parametrize("name,P_l", [("tiny", 4), ("small", 8)])
+def test_lockstep_with_appended_batches(name, P_l):
+    """Expansion input (a16): after every progress-free tick or mid-round prune
+    a batch is appended (S_mer = S_pr || S_app, own segments)."""
+    F, shape, gp, op, xo, xg = _pair(name, max_ctx=1024, prefix_len=24)
+    rng = gen.Rng(77)
+    appended = [0]
+
+    def append(r, ticks, gp_, op_):
+        if not op_.live or len(op_.node) + 6 > 200 or appended[0] >= 12:
+            return
+        parent, token, own = _append_batch(op_, rng, 6, shape.vocab)
+        so = op_.submit(False, parent, token, own, l_max=P_l)
+        sg = gp_.fs_submit_segment(F.FS_APPEND, parent, token, own, P_l)
+        assert sg["order"] == so["order"] and sg["bounds"] == [tuple(b) for b in so["bounds"]]
+        appended[0] += 1
+
+    st = run_lockstep(gp, op, planted_trees(shape, 20, 5, (0, 1, 3, 9), SEED), n_rounds=4,
+                      l_max=P_l, tol=1e-4 if not shape.bf16 else 2e-2, append_fn=append)
+    assert appended[0] > 0
+
+
+def test_error_codes_leave_state_unchanged():
+    F, shape, gp, op, xo, xg = _pair("tiny")
+
+    def state():
+        s = gp.state()
+        s.pop("launches")
+        return s
+
+    before = state()
+
+    def rc(f, *a):
+        try:
+            f(*a)
+        except F.FlowSpecError as e:
+            return e.code
+        return 0
+
+    x = before["x_new"]
+    # root token != x_new, non-topological parent, duplicate siblings, own outside (0,1]
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1, 0], [x + 1, 3], [1.0, 0.5], 4) == F.FS_EINVAL
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1, 2, 0], [x, 3, 4], [1.0, 0.5, 0.5], 4) == F.FS_EINVAL
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1, 0, 0], [x, 3, 3], [1.0, 0.5, 0.5], 4) == F.FS_EINVAL
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1, 0], [x, 3], [1.0, 1.5], 4) == F.FS_EINVAL
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1, 0], [x, 3], [1.0, 0.5], 0) == F.FS_EINVAL
+    assert rc(gp.fs_submit_segment, F.FS_APPEND, [0], [3], [0.5], 4) == F.FS_ESTATE
+    assert state() == before
+    # a valid round; then NEW_ROUND while live, APPEND with a pruned/unknown parent
+    gp.fs_submit_segment(F.FS_NEW_ROUND, [-1, 0, 0], [x, 3, 4], [1.0, 0.5, 0.4], 4)
+    assert rc(gp.fs_submit_segment, F.FS_NEW_ROUND, [-1], [x], [1.0], 4) == F.FS_ESTATE
+    assert rc(gp.fs_submit_segment, F.FS_APPEND, [99], [5], [0.5], 4) == F.FS_EINVAL
+    # inconsistent decisions are rejected without touching the state
+    s1 = state()
+    assert rc(gp.fs_prune_and_compact, dict(acc_ids=[1], x_new=0, n_new_id=-1, cont=0)) == F.FS_ESTATE
+    assert rc(gp.fs_prune_and_compact, dict(acc_ids=[0], x_new=0, n_new_id=7, cont=1)) == F.FS_ESTATE
+    assert state() == s1
+    o = gp.fs_verify_step()
+    assert o["n_rows"] == 3
