@@ -77,6 +77,11 @@ typedef struct fs_ctx fs_ctx;
  * block, KV cache, activations, tree state, workspaces).  0 if cfg invalid. */
 size_t fs_arena_bytes(const fs_config* cfg);
 
+/* Host only.  Layers per stage the configuration uses (cfg->layers_per_stage,
+ * or the byte-balanced consecutive blocks, head bytes counted on the last
+ * stage).  out: n_stages entries.  FS_EINVAL if invalid. */
+int fs_layers_per_stage(const fs_config* cfg, int32_t* out);
+
 /* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast it). */
 int fs_nccl_unique_id(uint8_t* out);
 

@@ -36,9 +36,13 @@ class Seg:
 
 class OraclePipeline:
     def __init__(self, shape, seed, n_stages=1, layers_per_stage=None, max_slots=4096,
-                 max_live=512, cache_weights=False, keep_logits=True):
+                 max_live=512, cache_weights=False, keep_logits=True, rank=None):
         self.shape = shape
         self.P = n_stages
+        # SPMD mode (rank given): this process computes only stage `rank`; hidden
+        # rows move p -> p+1 by torch.distributed send/recv and the last stage's
+        # per-row (argmax, margin) is broadcast — the protocol of fs_verify_step.
+        self.rank = rank
         if layers_per_stage is None:
             base, rem = divmod(shape.n_layers, n_stages)
             layers_per_stage = [base + (1 if p < rem else 0) for p in range(n_stages)]
@@ -227,6 +231,8 @@ class OraclePipeline:
         stage's output is verified, segments shift one stage."""
         if self.queue and self.slot[0] is None:
             self.slot[0] = self.queue.pop(0)
+        if self.rank is not None:
+            return self._verify_step_spmd()
         depth, anc = self._derived()
         out = dict(seg_id=-1, s_begin=0, n_rows=0, node=[], am=[], margin=[], logits=None)
         for p in range(self.P):
@@ -258,6 +264,58 @@ class OraclePipeline:
         for p in range(self.P - 1, 0, -1):
             self.slot[p] = self.slot[p - 1]
         self.slot[0] = None
+        return out
+
+    def _verify_step_spmd(self):
+        import torch
+        import torch.distributed as dist
+        depth, anc = self._derived()
+        p, P, d = self.rank, self.P, self.shape.d_model
+        out = dict(seg_id=-1, s_begin=0, n_rows=0, node=[], am=[], margin=[], logits=None)
+        seg = self.slot[p]
+        last = p == P - 1
+        if seg is not None and seg.e > seg.b:
+            rows, toks, pos, slot, vis = self._rows(seg, depth, anc)
+            h, lg = fso.forward(self.model, self.kv, self.lb[p], self.le[p], toks, pos, slot, vis,
+                                h_in=seg.h, want_hidden=not last, want_logits=last)
+            seg.h = h
+            if last:
+                res = torch.tensor([T.argmax_margin(lg[k]) for k in range(len(rows))],
+                                   dtype=torch.float64)
+                out["logits"] = lg
+        # stage handoff: p sends its rows to p+1, receives p-1's rows
+        prev = self.slot[p - 1] if p > 0 else None
+        recv_h = None
+        if p < P - 1 and seg is not None and seg.e > seg.b:
+            dist.send(torch.from_numpy(np.ascontiguousarray(seg.h)), dst=p + 1)
+        if prev is not None and prev.e > prev.b:
+            recv_h = torch.empty((prev.e - prev.b, d), dtype=torch.float32)
+            dist.recv(recv_h, src=p - 1)
+        # the last stage's (argmax, margin) rows reach every replica
+        oseg = self.slot[P - 1]
+        if oseg is not None and oseg.e > oseg.b:
+            n = oseg.e - oseg.b
+            if not last:
+                res = torch.empty((n, 2), dtype=torch.float64)
+            dist.broadcast(res, src=P - 1)
+            for k in range(n):
+                i = oseg.b + k
+                self.verified[i] = True
+                self.am[i] = int(res[k, 0])
+                self.margin[i] = float(res[k, 1])
+            out.update(seg_id=oseg.seg_id, s_begin=oseg.b, n_rows=n,
+                       node=[self.node[oseg.b + k] for k in range(n)],
+                       am=[int(res[k, 0]) for k in range(n)], margin=[float(res[k, 1]) for k in range(n)])
+        elif oseg is not None:
+            out.update(seg_id=oseg.seg_id, s_begin=oseg.b, n_rows=0)
+        for q in range(P):
+            if self.slot[q] is not None:
+                self.n_cached[q] = max(self.n_cached[q], self.slot[q].e)
+        for q in range(P - 1, 0, -1):
+            self.slot[q] = self.slot[q - 1]
+        self.slot[0] = None
+        if p > 0 and self.slot[p] is not None:
+            self.slot[p].h = recv_h.numpy() if recv_h is not None else None
         return out
 
     # ------------------------------------------------------------ accept

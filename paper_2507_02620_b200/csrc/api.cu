@@ -845,6 +845,14 @@ size_t fs_arena_bytes(const fs_config* cfg) {
   return carve(&tmp, nullptr);
 }
 
+int fs_layers_per_stage(const fs_config* cfg, int32_t* out) {
+  if (!out || !cfg_valid(cfg, nullptr)) return FS_EINVAL;
+  int lps[FS_MAX_STAGES];
+  balance(cfg, lps);
+  for (int p = 0; p < cfg->n_stages; p++) out[p] = lps[p];
+  return FS_OK;
+}
+
 int fs_nccl_unique_id(uint8_t* out) {
   if (!out) return FS_EINVAL;
   ncclUniqueId id;

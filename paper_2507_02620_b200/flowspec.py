@@ -62,7 +62,7 @@ class fs_profile(C.Structure):
                 ("attn_launches", C.c_uint64), ("attn_ms", C.c_double), ("attn_bytes", C.c_double)]
 
 
-EXPORTS = ["fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
+EXPORTS = ["fs_layers_per_stage", "fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
            "fs_last_error", "fs_strerror"]
@@ -83,6 +83,7 @@ def lib():
         L.fs_arena_bytes.restype = C.c_size_t
         L.fs_arena_bytes.argtypes = [C.POINTER(fs_config)]
         L.fs_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.fs_layers_per_stage.argtypes = [C.POINTER(fs_config), C.POINTER(i32)]
         L.fs_init.argtypes = [C.POINTER(fs_config), C.POINTER(P)]
         L.fs_load_random_weights.argtypes = [P, C.c_uint64]
         L.fs_set_prefix.argtypes = [P, ip, i32, i32, C.c_uint64, ip]
@@ -299,6 +300,15 @@ class Pipeline:
         self._chk(self.L.fs_read_kv(self.h, layer, which, kvh, slot,
                                     out.ctypes.data_as(C.POINTER(C.c_float))), "fs_read_kv")
         return out
+
+
+def layers_per_stage(shape, n_stages):
+    cfg = make_config(shape, n_stages=n_stages, max_ctx=4096)
+    out = (i32 * n_stages)()
+    rc = lib().fs_layers_per_stage(C.byref(cfg), out)
+    if rc != FS_OK:
+        raise FlowSpecError(rc, "fs_layers_per_stage")
+    return list(out)
 
 
 def nccl_unique_id():

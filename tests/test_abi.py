@@ -83,3 +83,26 @@ def test_no_oracle_in_product_path():
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower().replace("oracle/", ""), f
     so = open(os.path.join(pkg, "libflowspec.so"), "rb").read()
     assert b"fso_" not in so
+
+
+def test_layer_partition_byte_balanced(fsmod):
+    """Consecutive layer blocks balanced by bytes with the head on the last
+    stage: 7B P=4 -> 8/8/8/8; 72B P=8 -> the last stage (head =
+    1.37 layers of bytes) gets the fewest layers."""
+    from synth.configs import SHAPES
+    assert fsmod.layers_per_stage(SHAPES["7b"], 1) == [32]
+    assert fsmod.layers_per_stage(SHAPES["7b"], 4) == [8, 8, 8, 8]
+    for name in ("7b", "13b", "72b"):
+        s = SHAPES[name]
+        layer = (s.d_model * (s.n_heads + 2 * s.n_kv_heads) * s.head_dim
+                 + s.n_heads * s.head_dim * s.d_model + 3 * s.d_model * s.ffn)
+        head = s.vocab * s.d_model
+        for P in (2, 4, 8):
+            lps = fsmod.layers_per_stage(s, P)
+            assert sum(lps) == s.n_layers and min(lps) >= 1
+            load = [l * layer for l in lps]
+            load[-1] += head
+            # no single-layer move improves the most loaded stage
+            assert max(load) - min(load) <= layer + head
+    l72 = fsmod.layers_per_stage(SHAPES["72b"], 8)
+    assert l72[-1] == min(l72)
