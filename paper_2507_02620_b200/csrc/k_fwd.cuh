@@ -431,6 +431,7 @@ __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks) {
 constexpr int ATT_SUB = 64;   // keys per sub-chunk
 constexpr int ATT_NBUF = 3;   // sub-chunk ring depth
 constexpr int ATT_MAXQR = 32;
+constexpr int ATT_SO_LD = ATT_HD + 4;   // padded row of the key-warp state scratch
 
 struct AttnMhaArgs {
   AttnArgs a;
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   bf16* sQ = reinterpret_cast<bf16*>(att_smem);
   bf16* sKV = sQ + (size_t)QR * ATT_LD;
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(sKV + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD);
-  float* sPart = reinterpret_cast<float*>(sKV) + 4 * 16 * ATT_HD + 4 * 16 * 2;
+  float* sPart = reinterpret_cast<float*>(sKV) + 4 * 16 * ATT_SO_LD + 4 * 16 * 2;
   float* sPml = sPart + ATT_MAXQR * ATT_HD;
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   // keys of this split; rows/sizes are written before the tick's first kernel
@@ -487,20 +488,22 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   int issued = 0;
   while (issued < npre && kbeg + (issued + 1) * ATT_SUB <= first_written) load_sub(issued++);
   const int n_early = issued;   // sub-chunk groups committed before the Q group
-  pdl_wait();
+  // row descriptor and ancestor bitsets are written before the tick's first
+  // kernel (tick setup / submit / prune): stage them before the dependency too
   const int n_rows = rows->n_rows;
-  // Q (GQA-packed rows) and the ancestor rows: one cp.async group
+  for (int idx = tid; idx < a.npad * a.ancw; idx += 128) {
+    const int m = idx / a.ancw, w = idx % a.ancw;
+    const int s = (m < n_rows) ? rows->sidx[m] : -1;
+    sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
+  }
+  pdl_wait();
+  // Q (GQA-packed rows): one cp.async group
   for (int idx = tid; idx < QR * (ATT_HD / 8); idx += 128) {
     const int r = idx / (ATT_HD / 8), c = idx % (ATT_HD / 8);
     const int g = r / a.npad, m = r % a.npad;
     cp_async16(sQ + (size_t)r * ATT_LD + c * 8, a.q + ((size_t)m * a.H + kvh * G + g) * ATT_HD + c * 8);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int idx = tid; idx < a.npad * a.ancw; idx += 128) {
-    const int m = idx / a.ancw, w = idx % a.ancw;
-    const int s = (m < n_rows) ? rows->sidx[m] : -1;
-    sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
-  }
   while (issued < npre) load_sub(issued++);
   pdl_trigger();
   ATT_PROBE(1);
@@ -519,6 +522,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   for (int j = 0; j < 16; j++) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   constexpr int NT8 = KPW / 8;
+  uint32_t qf[ATT_HD / 16][4];
   // groups committed so far: pre-dependency sub-chunks, Q, remaining prefetch;
   // wait until sub-chunk sc and Q have landed
   for (int sc = 0; sc < nsc; sc++) {
@@ -536,18 +540,22 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     const bf16* sV = sK + ATT_SUB * ATT_LD;
     const int kb = ks * KPW;
     const int key0 = kbeg + sc * ATT_SUB + kb;
+    if (sc == 0) {  // Q fragments of this m-tile stay in registers for every sub-chunk
+#pragma unroll
+      for (int kk = 0; kk < ATT_HD / 16; kk++)
+        ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3],
+                sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
+    }
     float sacc[NT8][4];
 #pragma unroll
     for (int j = 0; j < NT8; j++) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
 #pragma unroll
     for (int kk = 0; kk < ATT_HD / 16; kk++) {
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4(a0, a1, a2, a3, sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
 #pragma unroll
       for (int j = 0; j < NT8; j++) {
         uint32_t b0, b1;
         ldsm_x2(b0, b1, sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8);
-        mma_bf16_16816(sacc[j], a0, a1, a2, a3, b0, b1);
+        mma_bf16_16816(sacc[j], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
       }
     }
     float mnew[2] = {mrow[0], mrow[1]};
@@ -626,14 +634,14 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   }
   ATT_PROBE(10);
   // ---- merge the KS key-warps of each m-tile (shared memory)
-  float* so = reinterpret_cast<float*>(sKV);                  // [4][16][HD]
-  float* sml = so + 4 * 16 * ATT_HD;                          // [4][16][2]
+  float* so = reinterpret_cast<float*>(sKV);                  // [4][16][SO_LD] (padded rows)
+  float* sml = so + 4 * 16 * ATT_SO_LD;                       // [4][16][2]
   __syncthreads();
   for (int h2 = 0; h2 < 2; h2++) {
     const int r16 = g_row + 8 * h2;
 #pragma unroll
     for (int j = 0; j < 16; j++)
-      *reinterpret_cast<float2*>(so + ((size_t)warp * 16 + r16) * ATT_HD + j * 8 + t4 * 2) =
+      *reinterpret_cast<float2*>(so + ((size_t)warp * 16 + r16) * ATT_SO_LD + j * 8 + t4 * 2) =
           make_float2(oacc[j][2 * h2], oacc[j][2 * h2 + 1]);
     if (t4 == 0) {
       sml[(warp * 16 + r16) * 2] = mrow[h2];
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
       const int w = m2 + MT * k2;
       const float wt = (mm[k2] == -INFINITY) ? 0.f : exp2f(mm[k2] - M);
       L += sml[(w * 16 + r16) * 2 + 1] * wt;
-      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)w * 16 + r16) * ATT_HD + d0);
+      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)w * 16 + r16) * ATT_SO_LD + d0);
 #pragma unroll
       for (int u = 0; u < 4; u++) {
         const float4 o = src[u];

@@ -51,6 +51,7 @@ SHAPES = {
     # full per-layer shapes of 7B / 72B with 2 layers (oracle-cheap parity)
     "7b_l2": Shape(2, 4096, 32, 32, 128, 11008, 32000, 0, 1, 1e-5, 1e4),
     "72b_l2": Shape(2, 8192, 64, 8, 128, 29568, 152064, 1, 1, 1e-6, 1e6),
+    "13b_l2": Shape(2, 5120, 40, 40, 128, 13824, 32000, 0, 1, 1e-5, 1e4),
 }
 
 

@@ -1,0 +1,48 @@
+"""Per-layer shapes of BASELINE.json configs[3] (13B) and configs[4] (Qwen2-72B:
+GQA 64/8, q/k/v bias, 32-row segments, long synthetic-KV context) with two
+layers, in lockstep with the oracle (every S order / mask / prune / KV slot map
+bit-exact, logits within 2e-2, accepted tokens identical except flagged)."""
+import numpy as np
+import pytest
+
+from oracle.pipeline import OraclePipeline
+from synth import gen
+from synth.configs import SHAPES
+from tests.lockstep import planted_trees, run_lockstep
+
+pytestmark = pytest.mark.gpu
+SEED = 0x5EED01
+
+
+def _run(name, prefix_len, mode, max_seg, l_max, n_nodes, depth, planted, max_ctx, n_rounds):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2507_02620_b200 import flowspec as F
+    shape = SHAPES[name]
+    gp = F.Pipeline(shape, max_ctx=max_ctx, max_seg=max_seg)
+    gp.fs_load_random_weights(SEED)
+    gp.enable_logits()
+    op = OraclePipeline(shape, SEED, max_slots=max_ctx)
+    prefix = gen.prefix_tokens(SEED, prefix_len, shape.vocab)
+    xo = op.set_prefix(prefix, mode=mode, kv_seed=7)
+    xg = gp.fs_set_prefix(prefix, F.FS_SYNTH_KV if mode == "synth" else F.FS_PREFILL, kv_seed=7)
+    srt = np.sort(op.prefix_logits)
+    assert xg == xo or srt[-1] - srt[-2] < 1e-2
+    st = run_lockstep(gp, op, planted_trees(shape, n_nodes, depth, planted, SEED), n_rounds=n_rounds,
+                      l_max=l_max, tol=2e-2)
+    print(f"{name}: max|dlogit| {st.max_abs:.3e} rows {st.rows} flagged {st.flagged} "
+          f"overrides {st.overrides} committed {len(st.committed)}")
+    return st
+
+
+def test_13b_layers_expansion_shapes():
+    """configs[3] per-layer shapes (d 5120, 40 heads, ffn 13824), 16-row segments."""
+    _run("13b_l2", 300, "synth", 16, 16, 64, 6, (0, 2, 5, 17, 21), 1024, 2)
+
+
+def test_72b_layers_gqa_bias_32row_segments_long_context():
+    """configs[4] per-layer shapes: GQA 64/8 (8 query heads per KV head packed into
+    M = 8 x 32 rows), q/k/v bias, 32-row segments (UMMA N = 64), 16K-token
+    synthetic-KV context (130 attention chunks), 256-node trees."""
+    _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
