@@ -75,6 +75,11 @@ struct fs_ctx {
   int P = 1, rank = 0, L0 = 0, L1 = 0, nl = 0;
   bool first = true, last = true, bf = true;
   int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536, gemm_ctas = 2;
+  // L2 prefetch budgets (MB) after QKV / O / gate-up / down: off by default --
+  // measured on the 7B stage: the prefetch traffic slows the latency-bound
+  // attention more than it shortens the next mainloop
+  double pf_mb[4] = {0, 0, 0, 0};
+  int att_dbg_ends = 0;
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   // arena
@@ -455,8 +460,37 @@ void prof_end(fs_ctx* c, int idx) {
 }
 
 // ---------------------------------------------------------------- launches
+// L2 prefetch plan for the GEMM that follows `g` (DESIGN.md "L2 weight
+// prefetch"): the leading `budget` bytes of nx's weights in nx's own
+// consumption order, skipping the boxes nx's CTAs load into shared memory
+// themselves before their grid dependency resolves
+PfPlan make_pf(const GemmOp* nx, double budget, int stages) {
+  PfPlan p;
+  memset(&p, 0, sizeof(p));
+  if (!nx || budget <= 0) return p;
+  p.kind = nx->split > 0 ? 1 : 2;
+  p.T = nx->sh.n_tiles;
+  p.S = nx->split;
+  p.KB = nx->sh.kb_total;
+  p.U = nx->sh.units;
+  p.G = nx->grid;
+  const int n_cons = p.kind == 1 ? p.T * p.S : p.G;
+  const int per = p.kind == 1 ? p.KB / std::max(1, p.S) : p.U / std::max(1, p.G);
+  p.skip = std::min(stages, per);
+  p.depth = std::min(per - p.skip, (int)(budget / ((double)n_cons * 128 * 64 * 2)));
+  if (p.depth <= 0) p.kind = 0;
+  return p;
+}
+
+double pf_budget(const char* env, double def_mb) {
+  const char* v = getenv(env);
+  return (v ? atof(v) : def_mb) * 1e6;
+}
+
 template <int NT>
-int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
+int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* nx, double pf_bytes) {
+  const PfPlan pf = make_pf(nx, pf_bytes, GemmCfg<NT>::STAGES);
+  const CUtensorMap& tmP = (pf.kind && nx) ? nx->ta : g.ta;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,7 +521,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
     at[1].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 2;
-    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, sh, ep);
+    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, tmP, sh, ep, pf);
     CK_LAUNCH(c);
     return FS_OK;
   }
@@ -509,20 +543,21 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaLaunchKernelEx(&lc, gemm_tc_kernel<NT>, g.ta, g.tb, sh, ep);
+  cudaLaunchKernelEx(&lc, gemm_tc_kernel<NT>, g.ta, g.tb, tmP, sh, ep, pf);
   CK_LAUNCH(c);
   return FS_OK;
 }
 
-int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
+int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* nx = nullptr,
+                double pf_bytes = 0) {
   const double bytes = (double)g.sh.n_out * g.sh.K * 2 + 2.0 * c->npad * g.sh.K * 2 +
                        (double)c->h_rows->n_rows * g.sh.n_out * 4;
   const int pi = prof_begin(c, 0, bytes);
   int rc;
   switch (c->npad) {
-    case 16: rc = launch_gemm_nt<16>(c, g, ep); break;
-    case 32: rc = launch_gemm_nt<32>(c, g, ep); break;
-    default: rc = launch_gemm_nt<64>(c, g, ep); break;
+    case 16: rc = launch_gemm_nt<16>(c, g, ep, nx, pf_bytes); break;
+    case 32: rc = launch_gemm_nt<32>(c, g, ep, nx, pf_bytes); break;
+    default: rc = launch_gemm_nt<64>(c, g, ep, nx, pf_bytes); break;
   }
   prof_end(c, pi);
   return rc;
@@ -587,6 +622,7 @@ int launch_attention(fs_ctx* c, int l) {
     a.n_chunk_cap = c->att_chunk_cap;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
     a.dbg = c->att_dbg;
+    a.dbg_ends = c->att_dbg_ends;
     if (c->tl_buf) {
       a.dbg = c->tl_buf + c->tl_names.size() * 8192;
       c->tl_names.push_back("attn");
@@ -664,7 +700,10 @@ int layer_forward(fs_ctx* c, int l) {
     e.q_out = (bf16*)c->q;
     e.k_cache = (bf16*)kv_plane(c, l, 0);
     e.v_cache = (bf16*)kv_plane(c, l, 1);
-    if ((rc = launch_gemm(c, w.qkv, e))) return rc;
+    e.kv_prefetch = getenv("FS_NO_KV_PF") ? 0 : 1;
+    // L2 prefetch of the next GEMM's leading weights (keeps HBM busy across
+    // epilogues, transitions and attention); budgets in MB, env-tunable
+    if ((rc = launch_gemm(c, w.qkv, e, &w.o, pf_budget("FS_PF_QKV", c->pf_mb[0])))) return rc;
     if ((rc = launch_attention(c, l))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
@@ -672,11 +711,11 @@ int layer_forward(fs_ctx* c, int l) {
     e.ssq_out = c->ssq;
     e.z_gain = (const bf16*)w.g2;
     e.z_out = (bf16*)c->y;
-    if ((rc = launch_gemm(c, w.o, e))) return rc;
+    if ((rc = launch_gemm(c, w.o, e, &w.gu, pf_budget("FS_PF_O", c->pf_mb[1])))) return rc;
     e = norm_input(c);
     e.mode = EPI_GLU;
     e.act = (bf16*)c->act;
-    if ((rc = launch_gemm(c, w.gu, e))) return rc;
+    if ((rc = launch_gemm(c, w.gu, e, &w.dn, pf_budget("FS_PF_GU", c->pf_mb[2])))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
     e.x = c->x;
@@ -684,7 +723,8 @@ int layer_forward(fs_ctx* c, int l) {
     e.ssq_out = gn ? c->ssq : nullptr;
     e.z_gain = gn;
     e.z_out = gn ? (bf16*)c->y : nullptr;
-    if ((rc = launch_gemm(c, w.dn, e))) return rc;
+    const GemmOp* nx = (l + 1 < c->nl) ? &c->lw[l + 1].qkv : (c->last ? &c->head : nullptr);
+    if ((rc = launch_gemm(c, w.dn, e, nx, pf_budget("FS_PF_DN", c->pf_mb[3])))) return rc;
   } else {
     float* yf = c->yf;
     rmsnorm_kernel<float, float, false><<<np, 128, 0, c->st>>>(c->x, (const float*)w.g1, (float*)c->y, d,
@@ -1436,6 +1476,73 @@ int fs_get_profile(fs_ctx* c, fs_profile* out) {
 int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
   int rc;
   if (!check(c, &rc)) return rc;
+  if (kind == 9 || kind == 10) {
+    // diagnostics: phase probes of attention (9) or O-projection GEMM with its
+    // residual epilogue (10) launches running alone
+    const size_t per = 8192, nl = 8;
+    CK_CUDA(c, cudaMalloc(&c->tl_buf, per * nl * 8));
+    cudaMemsetAsync(c->tl_buf, 0, per * nl * 8, c->st);
+    c->tl_names.clear();
+    rc = FS_OK;
+    for (int i = 0; i < 6 && rc == FS_OK; i++) {
+      c->att_dbg_ends = i >= 4;   // launches 4, 5: end probes only (probe cost check)
+      if (kind == 9) {
+        rc = launch_attention(c, 0);
+      } else {
+        GemmEpi e = base_epi(c);
+        e.mode = EPI_RESID;
+        e.x = c->x;
+        e.ssq_out = c->ssq;
+        e.z_gain = (const bf16*)c->lw[0].g2;
+        e.z_out = (bf16*)c->y;
+        rc = launch_gemm(c, c->lw[0].o, e);
+      }
+      cudaStreamSynchronize(c->st);
+    }
+    c->att_dbg_ends = 0;
+    std::vector<unsigned long long> h(per * nl);
+    cudaMemcpyAsync(h.data(), c->tl_buf, h.size() * 8, cudaMemcpyDeviceToHost, c->st);
+    cudaStreamSynchronize(c->st);
+    cudaFree(c->tl_buf);
+    c->tl_buf = nullptr;
+    for (size_t i = 2; i < c->tl_names.size() && i < nl; i++) {
+      unsigned long long t00 = ~0ull;
+      for (size_t cta = 0; cta < 512; cta++) {
+        const unsigned long long v = h[i * per + cta * 16];
+        if (v) t00 = std::min(t00, v);
+      }
+      {
+        double cyc = 0, ns = 0;
+        int n = 0;
+        for (size_t cta = 0; cta < 512; cta++) {
+          const unsigned long long* pr = &h[i * per + cta * 16];
+          if (pr[0] && pr[14] && pr[15]) {
+            cyc += (double)pr[15];
+            ns += (double)(pr[14] - pr[0]);
+            n++;
+          }
+        }
+        fprintf(stderr, "%s launch %zu (isolated): SM clock %.0f MHz over %d CTAs\n",
+                kind == 9 ? "attention" : "O-proj gemm", i, n ? cyc / ns * 1e3 : 0.0, n);
+      }
+      for (int k = 0; k < 15; k++) {
+        std::vector<double> vals;
+        for (size_t cta = 0; cta < 512; cta++) {
+          const unsigned long long v = h[i * per + cta * 16 + k];
+          if (v && v >= t00) vals.push_back((v - t00) / 1e3);
+        }
+        if (vals.empty()) continue;
+        std::sort(vals.begin(), vals.end());
+        fprintf(stderr, "      aprobe %2d: min %8.2f p10 %8.2f med %8.2f p90 %8.2f max %8.2f (n=%zu)\n", k,
+                vals[0], vals[vals.size() / 10], vals[vals.size() / 2], vals[vals.size() * 9 / 10],
+                vals.back(), vals.size());
+      }
+    }
+    c->tl_names.clear();
+    *us = 0;
+    *bytes = 0;
+    return rc;
+  }
   if (kind == 8) {
     // timeline of one (non-graph) stage forward: per probed launch, first CTA start and last
     // CTA end relative to the first launch's start
@@ -1483,8 +1590,7 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
           }
         }
         if (g && i >= 7 && i <= 11) {  // per-probe distribution over CTAs for one layer
-          for (int k = 0; k < 14; k++) {
-            if (k == 7 || (k >= 10)) continue;
+          for (int k = 0; k < 13; k++) {
             std::vector<double> vals;
             for (size_t cta = 0; cta < 512; cta++) {
               unsigned long long v = h[i * per + cta * 16 + k];
@@ -1504,7 +1610,7 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
     *bytes = 0;
     return rc;
   }
-  if (!c->weights || !c->prefixed || iters < 1 || !us || !bytes || kind < 0 || kind > 7)
+  if (!c->weights || !c->prefixed || iters < 1 || !us || !bytes || kind < 0 || kind > 7)  // 8-10: above
     return fail(c, FS_EINVAL, "bad bench request");
   if (kind <= 5 && !c->bf) return fail(c, FS_EINVAL, "bf16 path only");
   if (kind == 4 && !c->last) return fail(c, FS_EINVAL, "head lives on the last stage");

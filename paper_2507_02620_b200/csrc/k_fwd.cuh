@@ -203,6 +203,7 @@ struct AttnArgs {
   int ancw, max_live, H, Hkv, max_ctx, npad, n_chunk_cap;
   float scale_log2;     // log2(e) / sqrt(hd)
   unsigned long long* dbg;  // optional phase timestamps [cta][16] (diagnostics)
+  int dbg_ends;             // diagnostics: record only the first and last probe
 };
 FS_DEV unsigned long long gtimer() {
   unsigned long long t;
@@ -211,7 +212,7 @@ FS_DEV unsigned long long gtimer() {
 }
 #define ATT_PROBE(k)                                                               \
   do {                                                                             \
-    if (a.dbg && threadIdx.x == 0)                                                 \
+    if (a.dbg && threadIdx.x == 0 && (!a.dbg_ends || (k) == 0 || (k) == 14))      \
       a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();  \
   } while (0)
 
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   // context K/V below the first slot written this tick do not depend on the
   // previous kernel (PDL): stream them before the grid dependency resolves
   ATT_PROBE(0);
+  const long long clk0 = clock64();
   const int first_written = rows->slot[0];
   const int npre = min(nsc, ATT_NBUF);
   int issued = 0;
@@ -558,6 +560,10 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
         mma_bf16_16816(sacc[j], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
       }
     }
+    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: QK^T done
+      if (sacc[0][0] == 12345.f) a.dbg[1] = 0;
+      ATT_PROBE(5);
+    }
     float mnew[2] = {mrow[0], mrow[1]};
 #pragma unroll
     for (int j = 0; j < NT8; j++)
@@ -604,6 +610,10 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
       oacc[j][2] *= corr[1];
       oacc[j][3] *= corr[1];
     }
+    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: softmax done
+      if (sacc[0][0] + oacc[15][3] == 12345.f) a.dbg[1] = 0;
+      ATT_PROBE(6);
+    }
     // O += P V with P as a bf16 hi + lo pair (R18: fp32 softmax/accumulation)
 #pragma unroll
     for (int kk = 0; kk < KPW / 16; kk++) {
@@ -624,7 +634,12 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
         mma_bf16_16816(oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
       }
     }
+    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: PV done
+      if (oacc[0][0] + oacc[15][3] == 12345.f) a.dbg[1] = 0;
+      ATT_PROBE(7);
+    }
     __syncthreads();                                    // ring slot sc free
+    if (sc == 1) ATT_PROBE(8);
     if (issued < nsc) load_sub(issued++);
   }
 #pragma unroll
@@ -734,8 +749,12 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     }
   }
   ATT_PROBE(13);
-  cluster.sync();   // keep every CTA's shared memory alive until all reads are done
+  // keep every CTA's shared memory alive until all DSMEM reads are done (they
+  // were consumed before arriving): relaxed, the output stores need not drain
+  cluster_sync_relaxed();
   ATT_PROBE(14);
+  if (a.dbg && threadIdx.x == 0)   // diagnostics: SM cycles between probes 0 and 14
+    a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + 15] = (unsigned long long)(clock64() - clk0);
 }
 
 // ---------------------------------------------------------------- argmax

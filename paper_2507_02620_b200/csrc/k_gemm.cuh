@@ -36,6 +36,33 @@ struct GemmShape {
   int late_trigger; // diagnostics: trigger dependents at exit instead of at start
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (diagnostics)
 };
+// L2 prefetch of the NEXT GEMM's leading weight boxes, issued by this GEMM's
+// producer threads once their own last TMA load is out: HBM keeps streaming
+// through this kernel's epilogue, the kernel transition and (after QKV) the
+// attention kernel, and the next GEMM's mainloop starts from L2.  The boxes
+// follow the next GEMM's own consumption order (its work decomposition).
+struct PfPlan {
+  int kind;              // 0 none, 1 cluster split-K consumer, 2 stream-K consumer
+  int T, S, KB, U, G;    // consumer geometry: tiles, split, k-blocks/tile, units, grid
+  int skip, depth;       // per consumer CTA: units [skip, skip + depth) of its range
+};
+FS_DEV void issue_l2_prefetch(const CUtensorMap* tm, const PfPlan& pf, int c, int g_cur) {
+  if (pf.kind == 1) {
+    for (int j = c; j < pf.T * pf.S; j += g_cur) {
+      const int t = j / pf.S, r = j % pf.S;
+      const int kb0 = (int)((long long)r * pf.KB / pf.S), kb1 = (int)((long long)(r + 1) * pf.KB / pf.S);
+      const int e = min(kb1, kb0 + pf.skip + pf.depth);
+      for (int kb = kb0 + pf.skip; kb < e; kb++) tma_prefetch_l2_2d(tm, kb * 64, t * 128);
+    }
+  } else if (pf.kind == 2) {
+    for (int j = c; j < pf.G; j += g_cur) {
+      const int u0 = (int)((long long)j * pf.U / pf.G), u1 = (int)((long long)(j + 1) * pf.U / pf.G);
+      const int e = min(u1, u0 + pf.skip + pf.depth);
+      for (int u = u0 + pf.skip; u < e; u++) tma_prefetch_l2_2d(tm, (u % pf.KB) * 64, (u / pf.KB) * 128);
+    }
+  }
+}
+
 FS_DEV unsigned long long g_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -80,7 +107,27 @@ struct GemmEpi {
   float* ssq_out;           // [n_tiles][npad] or null
   const bf16* z_gain;       // g of the next RMSNorm, or null
   bf16* z_out;
+  // QKV: L2 prefetch of this layer's context K/V rows [0, slot of the first
+  // row) for the attention kernel that follows (HBM is idle during the
+  // epilogue and the kernel transition)
+  int kv_prefetch;
 };
+
+// the producer thread's share of the K/V context prefetch (16 KB pieces)
+FS_DEV void kv_l2_prefetch(const GemmEpi& ep, int c, int g_cur) {
+  const int n_ctx = ep.rows->slot[0];   // keys below the first slot written this tick
+  if (n_ctx <= 0) return;
+  const size_t head_bytes = (size_t)n_ctx * 128 * sizeof(bf16);
+  const int per_head = (int)((head_bytes + 16383) / 16384);
+  const int total = 2 * ep.Hkv * per_head;
+  for (int j = c; j < total; j += g_cur) {
+    const int hp = j / per_head, piece = j % per_head;
+    const bf16* base = (hp < ep.Hkv ? ep.k_cache : ep.v_cache) + (size_t)(hp % ep.Hkv) * ep.max_ctx * 128;
+    const size_t off = (size_t)piece * 16384;
+    const uint32_t len = (uint32_t)min((size_t)16384, head_bytes - off);
+    bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(base) + off, len);
+  }
+}
 
 // The activation operand carries each fp32 value as two bf16 rows (hi, lo:
 // rows [0,NT) and [NT,2NT) of the B tile), so UMMA N = 2*NT and the epilogue
@@ -112,21 +159,68 @@ FS_DEV int cta_of_unit(int u, int units, int G) {
   return (int)(((long long)(u + 1) * G + units - 1) / units) - 1;
 }
 
+// Epilogue operands that do not depend on the accumulator, loaded by the
+// epilogue warps while the mainloop streams (they idle until acc_full): the
+// dependent L2 round trips (n_rows -> pos -> rope, bias, slot, residual, gain)
+// then stay off the critical path between the last MMA and the stores.
+template <int NT>
+struct EpiPre {
+  static constexpr int NP = NT <= 16 ? NT : 1;   // register budget: NT=16 only
+  int n_rows;
+  bool tile;          // bias / gv / x hold tile t's values
+  float bias, gv;
+  float2 cs[NP];
+  int slot[NP];
+  float x[NP];
+};
+
+template <int NT, bool PFR = true>
+FS_DEV void epi_prefetch(const GemmShape& sh, const GemmEpi& ep, int t, int row, int mlo, int mhi,
+                         bool tile, EpiPre<NT>& p) {
+  const TickRows* rows = ep.rows;
+  p.n_rows = rows->n_rows;
+  p.tile = tile;
+  p.bias = 0.f;
+  p.gv = 0.f;
+  const int ng = t * 128 + row;
+  const int mend = min(mhi, p.n_rows);
+  if (ep.mode == EPI_QKV) {
+    if (tile && ep.bias) p.bias = to_f32(ep.bias[ng]);
+    if constexpr (PFR && NT <= 16) {
+      const int i = row & 63;
+#pragma unroll
+      for (int m = 0; m < NT; m++) {
+        const bool live = m >= mlo && m < mend;
+        p.slot[m] = live ? rows->slot[m] : 0;
+        p.cs[m] = live ? ep.rope[(size_t)rows->pos[m] * 64 + i] : make_float2(0.f, 0.f);
+      }
+    }
+  } else if (ep.mode == EPI_RESID) {
+    if (tile && ep.z_gain && ng < sh.n_out) p.gv = __bfloat162float(ep.z_gain[ng]);
+    if constexpr (PFR && NT <= 16) {
+#pragma unroll
+      for (int m = 0; m < NT; m++)
+        p.x[m] = (tile && m >= mlo && m < mend && ng < sh.n_out) ? ep.x[(size_t)m * ep.d + ng] : 0.f;
+    }
+  }
+}
+
 // Fused epilogue for output rows (weights) t*128+row; token columns m in
 // [mlo, mhi) are owned by this call (all NT for stream-K, a share in cluster
 // split-K), v[] holds the fp32 accumulator of every column.
-template <int NT>
+template <int NT, bool PFR = true>
 FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
-                          float* xch, Top2* stop, int mlo, int mhi, const float* xpre = nullptr) {
+                          float* xch, Top2* stop, int mlo, int mhi, const EpiPre<NT>& p) {
   const TickRows* rows = ep.rows;
-  const int n_rows = rows->n_rows;
+  const int n_rows = p.n_rows;
+  constexpr bool PF = PFR && NT <= 16;   // per-row operands prefetched (cluster kernel)
   const int ng = t * 128 + row;
   const int lane = lane_id(), q = warp_id() & 3;
   const int mend = min(mhi, n_rows);
   if (ep.mode == EPI_QKV) {
     const int H = ep.H, Hkv = ep.Hkv;
     if (ep.bias) {
-      const float b = to_f32(ep.bias[ng]);
+      const float b = p.tile ? p.bias : to_f32(ep.bias[ng]);
 #pragma unroll
       for (int m = 0; m < NT; m++) v[m] += b;
     }
@@ -140,7 +234,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       for (int m = 0; m < NT; m++) {
         const float pv = xch[(row ^ 64) * (NT + 1) + m];
         if (m >= mlo && m < mend) {
-          const float2 cs = ep.rope[(size_t)rows->pos[m] * 64 + i];
+          const float2 cs = PF ? p.cs[PF ? m : 0] : ep.rope[(size_t)rows->pos[m] * 64 + i];
           v[m] = (row < 64) ? (v[m] * cs.x - pv * cs.y) : (v[m] * cs.x + pv * cs.y);
         }
       }
@@ -153,9 +247,11 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       if (hh < H) {
         ep.q_out[((size_t)m * H + hh) * 128 + row] = o;
       } else if (hh < H + Hkv) {
-        ep.k_cache[((size_t)(hh - H) * ep.max_ctx + rows->slot[m]) * 128 + row] = o;
+        const int sl = PF ? p.slot[PF ? m : 0] : rows->slot[m];
+        ep.k_cache[((size_t)(hh - H) * ep.max_ctx + sl) * 128 + row] = o;
       } else {
-        ep.v_cache[((size_t)(hh - H - Hkv) * ep.max_ctx + rows->slot[m]) * 128 + row] = o;
+        const int sl = PF ? p.slot[PF ? m : 0] : rows->slot[m];
+        ep.v_cache[((size_t)(hh - H - Hkv) * ep.max_ctx + sl) * 128 + row] = o;
       }
     }
   } else if (ep.mode == EPI_GLU) {
@@ -180,7 +276,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 #pragma unroll
     for (int m = 0; m < NT; m++) {
       xn[m] = 0.f;
-      if (m >= mlo && m < mend && ng < sh.n_out) xn[m] = xpre ? xpre[m] : ep.x[(size_t)m * ep.d + ng];
+      if (m >= mlo && m < mend && ng < sh.n_out) xn[m] = (PF && p.tile) ? p.x[PF ? m : 0] : ep.x[(size_t)m * ep.d + ng];
     }
 #pragma unroll
     for (int m = 0; m < NT; m++) {
@@ -191,8 +287,9 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
         sq[m] = xn[m] * xn[m];
       }
     }
+    if (threadIdx.x == 64 && sh.dbg) GEMM_PROBE(10);
     if (ep.z_out && ng < sh.n_out) {  // next norm's B operand: x_new * g as a bf16 hi/lo pair
-      const float gv = __bfloat162float(ep.z_gain[ng]);
+      const float gv = p.tile ? p.gv : __bfloat162float(ep.z_gain[ng]);
 #pragma unroll
       for (int m = 0; m < NT; m++) {
         if (m < mlo || m >= mhi) continue;
@@ -202,6 +299,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
         ep.z_out[(size_t)(NT + m) * ep.d + ng] = __float2bfloat16_rn(zv - __bfloat162float(hi));
       }
     }
+    if (threadIdx.x == 64 && sh.dbg) GEMM_PROBE(11);
     if (ep.ssq_out) {  // deterministic per-tile sum of squares of the new residual rows
 #pragma unroll
       for (int m = 0; m < NT; m++) {
@@ -250,7 +348,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 template <int NT>
 __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   GemmShape sh, GemmEpi ep) {
+                   const __grid_constant__ CUtensorMap tmP, GemmShape sh, GemmEpi ep, PfPlan pfp) {
   using C = GemmCfg<NT>;
   extern __shared__ uint8_t gsm_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
@@ -275,6 +373,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (pfp.kind) tma_prefetch_desc(&tmP);
     for (int s = 0; s < C::STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -329,6 +428,8 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
           phase ^= 1;
         }
       }
+      issue_l2_prefetch(&tmP, pfp, c, G);
+      if (ep.kv_prefetch) kv_l2_prefetch(ep, c, G);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -371,9 +472,13 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    // previous kernels complete (their outputs are this epilogue's inputs, and
+    // their reads of this epilogue's outputs are done); then prefetch
+    pdl_wait();
+    EpiPre<NT> pf;
+    epi_prefetch<NT, false>(sh, ep, 0, row, 0, NT, false, pf);
     if (ep.scale_ssq) {
       // inv[m] of the RMSNorm applied by linearity (rows >= n_rows: padding)
-      pdl_wait();
       if (row < NT) {
         float ss = 0.f;
         for (int i = 0; i < ep.scale_n; i++) ss += ep.scale_ssq[(size_t)i * NT + row];
@@ -408,31 +513,44 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
         const int cf = cta_of_unit(t * KB, U, G);
         const int cl = cta_of_unit((t + 1) * KB - 1, U, G);
         const int j = c - cf, nc = cl - cf + 1;
-        float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
-#pragma unroll
-        for (int m = 0; m < NT; m += 4)
-          __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
-        // one gpu-scope release by the counting thread: bar.sync orders the other
-        // threads' partial stores before it (fence cumulativity)
+        // every other contributor already published (the common case for the CTA
+        // finishing a tile last): reduce from registers, no partial round trip
+        if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
         named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) {
-          __threadfence();
-          const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
-          if (last) __threadfence();   // acquire: every contributor's partial is visible
-          *s_flag = last;
+        const bool fast = *s_flag == 2;
+        if (!fast) {
+          float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
+#pragma unroll
+          for (int m = 0; m < NT; m += 4)
+            __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+          // one gpu-scope release by the counting thread: bar.sync orders the other
+          // threads' partial stores before it (fence cumulativity)
+          named_bar_sync(1, 128);
+          if (warp == 2 && lane == 0) {
+            __threadfence();
+            const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+            if (last) __threadfence();   // acquire: every contributor's partial is visible
+            *s_flag = last;
+          }
+          named_bar_sync(1, 128);
+          run_epi = *s_flag;
+        } else {
+          run_epi = true;
         }
-        named_bar_sync(1, 128);
-        run_epi = *s_flag;
         if (run_epi) {
+          float own[NT];
 #pragma unroll
-          for (int m = 0; m < NT; m++) v[m] = 0.f;
-          // partials summed in contributor order (deterministic); loads of up to
-          // four contributors are in flight together
+          for (int m = 0; m < NT; m++) {
+            own[m] = v[m];
+            v[m] = 0.f;
+          }
+          // partials summed in contributor order (deterministic, whichever CTA is
+          // last); loads of up to four contributors are in flight together
           for (int j0 = 0; j0 < nc; j0 += 4) {
             float4 pv[4][NT / 4];
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) {
-              if (j0 + jj < nc) {
+              if (j0 + jj < nc && j0 + jj != j) {
                 const float* rp = sh.ws + (((size_t)t * sh.max_contrib + j0 + jj) * 128 + row) * NT;
 #pragma unroll
                 for (int m = 0; m < NT / 4; m++) pv[jj][m] = __ldcg(reinterpret_cast<const float4*>(rp) + m);
@@ -441,12 +559,17 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 #pragma unroll
             for (int jj = 0; jj < 4; jj++) {
               if (j0 + jj < nc) {
+                if (j0 + jj == j) {
 #pragma unroll
-                for (int m = 0; m < NT / 4; m++) {
-                  v[4 * m] += pv[jj][m].x;
-                  v[4 * m + 1] += pv[jj][m].y;
-                  v[4 * m + 2] += pv[jj][m].z;
-                  v[4 * m + 3] += pv[jj][m].w;
+                  for (int m = 0; m < NT; m++) v[m] += own[m];
+                } else {
+#pragma unroll
+                  for (int m = 0; m < NT / 4; m++) {
+                    v[4 * m] += pv[jj][m].x;
+                    v[4 * m + 1] += pv[jj][m].y;
+                    v[4 * m + 2] += pv[jj][m].z;
+                    v[4 * m + 3] += pv[jj][m].w;
+                  }
                 }
               }
             }
@@ -461,7 +584,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 #pragma unroll
           for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
         }
-        gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, 0, NT);
+        gemm_epilogue<NT, false>(sh, ep, t, row, v, xch, stop, 0, NT, pf);
       }
       if (threadIdx.x == 64) GEMM_PROBE(9 + 2 * (seg & 1));
       u = seg_end;
@@ -489,7 +612,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 template <int NT>
 __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        GemmShape sh, GemmEpi ep) {
+                        const __grid_constant__ CUtensorMap tmP, GemmShape sh, GemmEpi ep, PfPlan pfp) {
   namespace cg = cooperative_groups;
   using C = GemmCfg<NT>;
   cg::cluster_group cluster = cg::this_cluster();
@@ -517,6 +640,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (pfp.kind) tma_prefetch_desc(&tmP);
     for (int s = 0; s < C::STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -531,6 +655,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   if (!sh.late_trigger) pdl_trigger();
+  EpiPre<NT> pf;
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: weights before the grid dependency, activations after
@@ -557,6 +682,8 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
           phase ^= 1;
         }
       }
+      issue_l2_prefetch(&tmP, pfp, blockIdx.x, gridDim.x);
+      if (ep.kv_prefetch) kv_l2_prefetch(ep, blockIdx.x, gridDim.x);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -587,90 +714,105 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   } else {
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    pdl_wait();
+    epi_prefetch<NT>(sh, ep, t, row, r * NT / S, (r + 1) * NT / S, true, pf);
+    if (threadIdx.x == 64 && sh.dbg) {  // diagnostics: prefetched operands have landed
+      float z = pf.gv + pf.bias;
+#pragma unroll
+      for (int m = 0; m < EpiPre<NT>::NP; m++) z += pf.x[m] + pf.cs[m].x + (float)pf.slot[m];
+      if (z == 12345.f) sh.dbg[0] = 0;
+      GEMM_PROBE(7);
+    }
     if (ep.scale_ssq) {
-      pdl_wait();
       if (row < NT) {
         float ss = 0.f;
         for (int i = 0; i < ep.scale_n; i++) ss += ep.scale_ssq[(size_t)i * NT + row];
         s_inv[row] = 1.0f / sqrtf(ss / (float)sh.K + ep.eps);
       }
     }
-    mbar_wait(&acc_full[0], 0);
-    tc_fence_after();
-    float v[NT];
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    // pass 0 runs the reduction + epilogue code on an empty column range while
+    // the mainloop streams: every global / DSMEM access is predicated off, the
+    // only effect is a warm instruction cache for pass 1 (the straight-line
+    // epilogue otherwise executes from cold i-cache lines, ~1 us per phase)
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+      if (pass == 1) {
+        mbar_wait(&acc_full[0], 0);
+        tc_fence_after();
+        float v[NT];
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll
-    for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
+        for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
 #pragma unroll
-    for (int j = 0; j < NT; j += 16) {
-      float w[16];
-      tmem_ld16(tl + NT + j, w);
+        for (int j = 0; j < NT; j += 16) {
+          float w[16];
+          tmem_ld16(tl + NT + j, w);
 #pragma unroll
-      for (int i = 0; i < 16; i++) v[j + i] += w[i];
-    }
-    // every MMA has completed (acc_full): the stage buffers are free for the partial
+          for (int i = 0; i < 16; i++) v[j + i] += w[i];
+        }
+        // every MMA has completed (acc_full): the stage buffers are free for the partial
 #pragma unroll
-    for (int m = 0; m < NT; m++) part[m * 128 + row] = v[m];
-  }
-  // residual values of my token columns, loaded before the barrier (RESID)
-  float xpre[NT];
-  if (warp >= 2 && ep.mode == EPI_RESID) {
-    const int row = (warp & 3) * 32 + lane;
-    const int ng = t * 128 + row;
-    const int mlo = r * NT / S, mhi = min((r + 1) * NT / S, ep.rows->n_rows);
+        for (int m = 0; m < NT; m++) part[m * 128 + row] = v[m];
+        cluster.sync();
+        if (threadIdx.x == 64) GEMM_PROBE(8);
+      }
+      const int mlo = r * NT / S, mhi = pass ? (r + 1) * NT / S : mlo;
+      float v[NT];
 #pragma unroll
-    for (int m = 0; m < NT; m++)
-      xpre[m] = (m >= mlo && m < mhi && ng < sh.n_out) ? ep.x[(size_t)m * ep.d + ng] : 0.f;
-  }
-  cluster.sync();
-  if (threadIdx.x == 64) GEMM_PROBE(8);
-  if (warp >= 2) {
-    const int row = (warp & 3) * 32 + lane;
-    const int mlo = r * NT / S, mhi = (r + 1) * NT / S;
-    float v[NT];
+      for (int m = 0; m < NT; m++) v[m] = 0.f;
+      // DSMEM partials of every rank for my columns: issue up to 4 ranks' loads
+      // together, accumulate in rank order (deterministic)
+      constexpr int MW = (NT + 1) / 2;   // max columns per rank (S >= 2)
+      float acc[MW];
 #pragma unroll
-    for (int m = 0; m < NT; m++) v[m] = 0.f;
-    // DSMEM partials of every rank for my columns: issue up to 4 ranks' loads
-    // together, accumulate in rank order (deterministic)
-    constexpr int MW = (NT + 1) / 2;   // max columns per rank (S >= 2)
-    float acc[MW];
+      for (int j = 0; j < MW; j++) acc[j] = 0.f;
+      for (int c0 = 0; c0 < S; c0 += 4) {
+        float pv[4][MW];
 #pragma unroll
-    for (int j = 0; j < MW; j++) acc[j] = 0.f;
-    for (int c0 = 0; c0 < S; c0 += 4) {
-      float pv[4][MW];
+        for (int cc = 0; cc < 4; cc++) {
+          if (c0 + cc < S) {
+            const uint32_t pc = dsmem_addr(part + mlo * 128 + row, (uint32_t)(c0 + cc));
 #pragma unroll
-      for (int cc = 0; cc < 4; cc++) {
-        if (c0 + cc < S) {
-          const uint32_t pc = dsmem_addr(part + mlo * 128 + row, (uint32_t)(c0 + cc));
+            for (int j = 0; j < MW; j++)
+              if (mlo + j < mhi) pv[cc][j] = ld_dsmem_f32(pc + j * 128 * 4);
+          }
+        }
 #pragma unroll
-          for (int j = 0; j < MW; j++)
-            if (mlo + j < mhi) pv[cc][j] = ld_dsmem_f32(pc + j * 128 * 4);
+        for (int cc = 0; cc < 4; cc++) {
+          if (c0 + cc < S) {
+#pragma unroll
+            for (int j = 0; j < MW; j++) acc[j] += (mlo + j < mhi) ? pv[cc][j] : 0.f;
+          }
         }
       }
-#pragma unroll
-      for (int cc = 0; cc < 4; cc++) {
-        if (c0 + cc < S) {
-#pragma unroll
-          for (int j = 0; j < MW; j++) acc[j] += (mlo + j < mhi) ? pv[cc][j] : 0.f;
-        }
+      if (threadIdx.x == 64 && sh.dbg) {  // diagnostics: DSMEM loads complete
+        if (acc[0] + acc[MW - 1] == 12345.f) sh.dbg[1] = 0;
+        GEMM_PROBE(9);
       }
+      // scatter acc[j] -> v[mlo + j] with static register indices
+#pragma unroll
+      for (int m = 0; m < NT; m++)
+#pragma unroll
+        for (int j = 0; j < MW; j++)
+          if (m == mlo + j && m < mhi) v[m] = acc[j];
+      if (threadIdx.x == 64 && sh.dbg) {
+        if (v[0] + v[NT - 1] == 12345.f) sh.dbg[1] = 0;
+        GEMM_PROBE(12);
+      }
+      if (ep.scale_ssq) {
+        named_bar_sync(1, 128);  // s_inv visible to all epilogue warps
+#pragma unroll
+        for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+      }
+      gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi, pf);
     }
-    if (threadIdx.x == 64) GEMM_PROBE(9);
-    // scatter acc[j] -> v[mlo + j] with static register indices
-#pragma unroll
-    for (int m = 0; m < NT; m++)
-#pragma unroll
-      for (int j = 0; j < MW; j++)
-        if (m == mlo + j && m < mhi) v[m] = acc[j];
-    if (ep.scale_ssq) {
-      named_bar_sync(1, 128);  // s_inv visible to all epilogue warps
-#pragma unroll
-      for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
-    }
-    gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi, ep.mode == EPI_RESID ? xpre : nullptr);
   }
+  // matches the epilogue warps' pass-1 barrier (these warps published nothing)
+  if (warp < 2) cluster_sync_relaxed();
   if (threadIdx.x == 64) GEMM_PROBE(5);
-  cluster.sync();   // peers are done reading this CTA's partial
+  // peers are done reading this CTA's partial (their DSMEM loads were consumed
+  // before they arrive): no release needed, the epilogue stores need not drain
+  cluster_sync_relaxed();
   if (threadIdx.x == 0) GEMM_PROBE(6);
   if (warp == 1) {
     tc_fence_after();

@@ -18,3 +18,7 @@ for k in range(8):
     print(f"{names[k]:12s} {us:9.2f} us  {by/1e6:8.2f} MB  {by/us/1e3 if us else 0:8.1f} GB/s")
 us, _ = gp.bench_kernel(8, 1)
 print("timeline stage span us", us)
+if "--attn" in sys.argv:
+    gp.bench_kernel(9, 1)
+if "--ogemm" in sys.argv:
+    gp.bench_kernel(10, 1)
