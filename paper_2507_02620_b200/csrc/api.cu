@@ -80,6 +80,7 @@ struct fs_ctx {
   // attention more than it shortens the next mainloop
   double pf_mb[4] = {0, 0, 0, 0};
   int att_dbg_ends = 0;
+  int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   // arena
@@ -635,9 +636,45 @@ int launch_attention(fs_ctx* c, int l) {
       AttnMhaArgs ma;
       ma.a = a;
       ma.out = (bf16*)c->att;
-      const int nsplit = 8;   // cluster of 8 key splits per kv head (sizes read on device)
       const size_t smem = (size_t)QR * ATT_LD * 2 + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD * 2 +
-                          (size_t)np * c->ancw * 4;
+                          (size_t)np * c->ancw * 4 + 16;
+      static bool mattr = false;
+      if (!mattr) {
+        cudaFuncSetAttribute(attn_mha_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        cudaFuncSetAttribute(attn_mha_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        mattr = true;
+      }
+      // cluster of key splits per kv head (sizes read on device): the largest
+      // split count <= 8 whose Hkv clusters are all co-resident (one wave;
+      // clusters must fit inside a GPC, so this is below 2 * SMs / Hkv)
+      if (c->att_nsplit[MT] == 0) {
+        int ns = 8;
+        for (; ns > 1; ns--) {
+          cudaLaunchConfig_t oc = {};
+          oc.gridDim = dim3(ns, Hkv);
+          oc.blockDim = dim3(128);
+          oc.dynamicSmemBytes = smem;
+          cudaLaunchAttribute oa[1];
+          oa[0].id = cudaLaunchAttributeClusterDimension;
+          oa[0].val.clusterDim.x = ns;
+          oa[0].val.clusterDim.y = 1;
+          oa[0].val.clusterDim.z = 1;
+          oc.attrs = oa;
+          oc.numAttrs = 1;
+          int nclu = 0;
+          const cudaError_t oe = MT == 1
+              ? cudaOccupancyMaxActiveClusters(&nclu, attn_mha_kernel<16>, &oc)
+              : cudaOccupancyMaxActiveClusters(&nclu, attn_mha_kernel<32>, &oc);
+          if (oe != cudaSuccess) {
+            cudaGetLastError();
+            ns = std::max(1, std::min(8, 2 * c->n_sms / std::max(1, Hkv)));
+            break;
+          }
+          if (nclu >= Hkv) break;
+        }
+        c->att_nsplit[MT] = ns;
+      }
+      const int nsplit = c->att_nsplit[MT];
       cudaLaunchConfig_t lc = {};
       lc.gridDim = dim3(nsplit, Hkv);
       lc.blockDim = dim3(128);
@@ -652,12 +689,6 @@ int launch_attention(fs_ctx* c, int l) {
       at[1].val.clusterDim.z = 1;
       lc.attrs = at;
       lc.numAttrs = 2;
-      static bool mattr = false;
-      if (!mattr) {
-        cudaFuncSetAttribute(attn_mha_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaFuncSetAttribute(attn_mha_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        mattr = true;
-      }
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 * 3);
       if (MT == 1)
         cudaLaunchKernelEx(&lc, attn_mha_kernel<16>, ma);

@@ -439,6 +439,12 @@ struct AttnMhaArgs {
   bf16* out;            // [2*npad][H*128] hi rows then lo rows
 };
 
+FS_DEV float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <int KPW>
 __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   namespace cg = cooperative_groups;
@@ -457,6 +463,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   bf16* sQ = reinterpret_cast<bf16*>(att_smem);
   bf16* sKV = sQ + (size_t)QR * ATT_LD;
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(sKV + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD);
+  int* sCtxMin = reinterpret_cast<int*>(sAnc + (size_t)a.npad * a.ancw);   // context floor of the live rows
   float* sPart = reinterpret_cast<float*>(sKV) + 4 * 16 * ATT_SO_LD + 4 * 16 * 2;
   float* sPml = sPart + ATT_MAXQR * ATT_HD;
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
@@ -498,6 +505,13 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     const int s = (m < n_rows) ? rows->sidx[m] : -1;
     sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
   }
+  if (warp == 0) {  // keys below every live row's context limit need no tree mask
+    int cm = 0x7fffffff;
+    for (int m = lane; m < n_rows; m += 32) cm = min(cm, rows->ctx_lim[m]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cm = min(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    if (lane == 0) *sCtxMin = cm;
+  }
   pdl_wait();
   // Q (GQA-packed rows): one cp.async group
   for (int idx = tid; idx < QR * (ATT_HD / 8); idx += 128) {
@@ -525,6 +539,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   constexpr int NT8 = KPW / 8;
   uint32_t qf[ATT_HD / 16][4];
+  int ctx_min = 0;
   // groups committed so far: pre-dependency sub-chunks, Q, remaining prefetch;
   // wait until sub-chunk sc and Q have landed
   for (int sc = 0; sc < nsc; sc++) {
@@ -537,7 +552,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     else if (allowed == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
     else asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    ATT_PROBE(2 + sc);
+    ATT_PROBE(2 + min(sc, 7));
     const bf16* sK = sKV + (size_t)(sc % ATT_NBUF) * 2 * ATT_SUB * ATT_LD;
     const bf16* sV = sK + ATT_SUB * ATT_LD;
     const int kb = ks * KPW;
@@ -547,6 +562,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
       for (int kk = 0; kk < ATT_HD / 16; kk++)
         ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3],
                 sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
+      ctx_min = *sCtxMin;
     }
     float sacc[NT8][4];
 #pragma unroll
@@ -565,22 +581,35 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
       ATT_PROBE(5);
     }
     float mnew[2] = {mrow[0], mrow[1]};
+    if (key0 + KPW <= min(kend, ctx_min)) {
+      // every key of this warp is context of every live row: no tree mask
+      // (padding rows produce finite values that are never written)
 #pragma unroll
-    for (int j = 0; j < NT8; j++)
+      for (int j = 0; j < NT8; j++)
 #pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int h2 = e >> 1;
-        const int key = key0 + j * 8 + t4 * 2 + (e & 1);
-        bool vis = key < kend && qm[h2] < n_rows;
-        if (vis && key >= ctx[h2]) {
-          const int aa = key - l_glo;
-          vis = sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
-                ((sAnc[qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+        for (int e = 0; e < 4; e++) {
+          const float v = sacc[j][e] * a.scale_log2;
+          sacc[j][e] = v;
+          mnew[e >> 1] = fmaxf(mnew[e >> 1], v);
         }
-        const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
-        sacc[j][e] = v;
-        mnew[h2] = fmaxf(mnew[h2], v);
-      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NT8; j++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int h2 = e >> 1;
+          const int key = key0 + j * 8 + t4 * 2 + (e & 1);
+          bool vis = key < kend && qm[h2] < n_rows;
+          if (vis && key >= ctx[h2]) {
+            const int aa = key - l_glo;
+            vis = sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
+                  ((sAnc[qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+          }
+          const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
+          sacc[j][e] = v;
+          mnew[h2] = fmaxf(mnew[h2], v);
+        }
+    }
 #pragma unroll
     for (int h2 = 0; h2 < 2; h2++) {
       mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 1));
@@ -589,7 +618,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     float corr[2], rs[2] = {0.f, 0.f};
 #pragma unroll
     for (int h2 = 0; h2 < 2; h2++) {
-      corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : exp2f(mrow[h2] - mnew[h2]);
+      corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : ex2_approx(mrow[h2] - mnew[h2]);
       mrow[h2] = mnew[h2];
     }
 #pragma unroll
@@ -597,7 +626,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
 #pragma unroll
       for (int e = 0; e < 4; e++) {
         const int h2 = e >> 1;
-        const float p = (sacc[j][e] == -INFINITY) ? 0.f : exp2f(sacc[j][e] - mrow[h2]);
+        const float p = (sacc[j][e] == -INFINITY) ? 0.f : ex2_approx(sacc[j][e] - mrow[h2]);
         sacc[j][e] = p;
         rs[h2] += p;
       }
