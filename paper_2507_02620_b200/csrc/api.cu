@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "k_fwd.cuh"
 #include "k_gemm.cuh"
+#include "k_attn_tc.cuh"
 #include "k_gen.cuh"
 #include "k_tree.cuh"
 #include "state.cuh"
@@ -65,6 +66,7 @@ struct LayerW {
   void *wqkv = nullptr, *bqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
   void *g1 = nullptr, *g2 = nullptr;
   GemmOp qkv, o, gu, dn;
+  CUtensorMap tk, tv;   // this layer's K / V cache planes [Hkv * max_ctx][128] (GQA tcgen05 attention)
 };
 
 }  // namespace
@@ -412,6 +414,8 @@ bool encode_map(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint3
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+char* kv_plane(fs_ctx* c, int local_layer, int which);
+
 bool build_maps(fs_ctx* c) {
   const fs_config& f = c->cfg;
   const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn;
@@ -428,6 +432,12 @@ bool build_maps(fs_ctx* c) {
     ok &= encode_map(&w.dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
 
     w.qkv.ok = w.o.ok = w.gu.ok = w.dn.ok = ok;
+  }
+  for (int l = 0; l < c->nl; l++) {
+    LayerW& w = c->lw[l];
+    const uint64_t kv_rows = (uint64_t)Hkv * f.max_ctx;
+    ok &= encode_map(&w.tk, kv_plane(c, l, 0), hd, kv_rows, 64, 128);
+    ok &= encode_map(&w.tv, kv_plane(c, l, 1), hd, kv_rows, 64, 128);
   }
   if (c->last) {
     ok &= encode_map(&c->head.ta, c->wh, d, f.vocab, 64, 128);
@@ -697,6 +707,42 @@ int launch_attention(fs_ctx* c, int l) {
       prof_end(c, api);
       CK_LAUNCH(c);
     } else {
+    if ((QR == 128 || QR == 256) && hd == ATT_HD && !getenv("FS_NO_TC_ATTN")) {
+      // grouped-query rows fill 128-row M-tiles: tcgen05 attention, one CTA per SM
+      const int nsplit = std::max(1, std::min(c->n_sms / Hkv, c->att_chunk_cap * 4));
+      TcAttnArgs ta;
+      ta.a = a;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(nsplit, Hkv);
+      lc.stream = c->st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
+                                           (double)nsplit * Hkv * QR * (hd + 2) * 4 * 2);
+      // P as a bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P_BF16)
+      const bool plo = getenv("FS_TC_ATTN_P_BF16") == nullptr;
+      auto go = [&](auto kern, int threads, int smem_bytes) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        lc.blockDim = dim3(threads);
+        lc.dynamicSmemBytes = smem_bytes;
+        cudaLaunchKernelEx(&lc, kern, c->lw[l].tk, c->lw[l].tv, ta);
+      };
+      if (QR == 128) {
+        if (plo) go(attn_gqa_tc_kernel<1, true>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
+        else go(attn_gqa_tc_kernel<1, false>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
+      } else {
+        if (plo) go(attn_gqa_tc_kernel<2, true>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
+        else go(attn_gqa_tc_kernel<2, false>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
+      }
+      prof_end(c, api);
+      CK_LAUNCH(c);
+      attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, 1, nsplit);
+      CK_LAUNCH(c);
+      return FS_OK;
+    }
     const int n_chunks = (n_keys + ATT_KC - 1) / ATT_KC;
     const size_t smem = (size_t)QR * ATT_LD * 2 + 2 * ATT_KC * ATT_LD * 2 + (size_t)np * c->ancw * 4;
     static bool attr = false;

@@ -1,0 +1,401 @@
+// k_attn_tc.cuh — GQA tree attention on 5th-gen tensor cores (tcgen05 + TMEM).
+//
+// For grouped-query configs (72B: G = 8 query heads per kv head) the G * npad
+// query rows of one kv head share every K/V row, so attention sits at the
+// ridge (256 flop/B at configs[4]) and belongs on the tensor
+// cores.  CTA = (key split, kv head), one CTA per SM:
+//   warp 0     TMA producer: K (and V) tiles of 128 keys, SWIZZLE_128B, 2 stages
+//   warp 1     MMA issuer (one thread): S = Q K^T into TMEM; O += P V from TMEM
+//   warps 2..  softmax: 4 warps per 128-row M-tile, one query row per thread
+// TMEM per M-tile: 128 columns S (fp32; P aliases it as bf16 hi | lo halves)
+// and 128 columns O.  Two passes over the split's keys: pass 1 computes the
+// row maxima M (S only), pass 2 recomputes S, writes P = 2^(s - M) as a bf16
+// hi/lo pair (PLO; precision contract R18, as the MHA kernel) or as bf16 (the
+// contract permits it) and accumulates O += P_hi V (+ P_lo V), so O never
+// needs rescaling.  K is read twice (the
+// second time mostly from L2).  The split's unnormalised O and (M, l) go to a
+// workspace that attn_combine_kernel merges in split order (deterministic).
+// Tree visibility (§8(a) a6): context keys [0, ctx_lim[m]) plus
+// ancestors-or-self of the row's node; key tiles below every live row's
+// context limit skip the mask.
+#pragma once
+#include "k_fwd.cuh"
+
+namespace fs {
+
+constexpr int TCA_KT = 128;              // keys per tile
+constexpr int TCA_BOX = 128 * 128;       // one SW128 box: 128 rows x 64 bf16 = 16 KB
+
+template <int MT2>
+struct TcAttnCfg {
+  static constexpr int THREADS = 64 + 256 * MT2;     // producer, MMA, 8 softmax warps per M-tile
+  static constexpr int Q_BYTES = MT2 * 2 * TCA_BOX;   // M-tiles x 2 head-dim boxes
+  static constexpr int STAGE_BYTES = 4 * TCA_BOX;     // K (2 boxes) | V (2 boxes)
+  static constexpr int NST = 2;
+  static constexpr int SMEM = 1024 + Q_BYTES + NST * STAGE_BYTES + 256 + 2048 + 4 * 128 * MT2;
+  static constexpr int TMEM_COLS = 256 * MT2;         // 256 or 512
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
+
+struct TcAttnArgs {
+  AttnArgs a;
+};
+
+FS_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// TMEM -> registers without the wait (the caller waits once for a batch)
+FS_DEV void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+FS_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+FS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// D[tmem] (+)= A[tmem] * B[smem]
+FS_DEV void umma_bf16_tmemA(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// shared-memory descriptor of an MN-major SWIZZLE_128B operand made of 64-wide
+// TMA boxes: LBO = distance between the boxes along MN, SBO = 8 rows along K
+// (validated by tools/micro/umma_mn_test.cu)
+FS_DEV uint64_t umma_sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+FS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int MT2, bool PLO>
+__global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
+    attn_gqa_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       TcAttnArgs args) {
+  using C = TcAttnCfg<MT2>;
+  const AttnArgs& a = args.a;
+  extern __shared__ uint8_t tsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + C::Q_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sKV + C::NST * C::STAGE_BYTES);
+  uint64_t* empty = full + C::NST;
+  uint64_t* s_full = empty + C::NST;     // [MT2]
+  uint64_t* p_full = s_full + 2;         // [MT2]
+  uint64_t* pv_done = p_full + 2;        // [MT2]: P V of the step complete (S/P columns free)
+  uint64_t* o_full = pv_done + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
+  int* sCtxMin = reinterpret_cast<int*>(tmem_holder + 1);
+  uint32_t* sAnc = reinterpret_cast<uint32_t*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256);
+  float* sHalf = reinterpret_cast<float*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256 + 2048);  // [QR] row max / sum exchange
+
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const int split = blockIdx.x, kvh = blockIdx.y, nsplit = gridDim.x;
+#define TCA_PROBE(k)                                                                       \
+  do {                                                                                     \
+    if (a.dbg && threadIdx.x == 64)                                                        \
+      a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();          \
+  } while (0)
+  TCA_PROBE(0);
+  const TickRows* rows = a.rows;
+  const int G = a.H / a.Hkv;
+  const int QR = G * a.npad;             // == 128 * MT2 (host-checked)
+  const int nk = rows->n_keys;
+  const int per = (nk + nsplit * TCA_KT - 1) / (nsplit * TCA_KT) * TCA_KT;
+  const int kbeg = min(nk, split * per);
+  const int kend = min(nk, kbeg + per);
+  const int T = (kend - kbeg + TCA_KT - 1) / TCA_KT;
+  float* ws_o = a.ws_o + ((size_t)split * a.Hkv + kvh) * QR * ATT_HD;
+  float* ws_ml = a.ws_ml + ((size_t)split * a.Hkv + kvh) * QR * 2;
+  if (T == 0) {   // empty split: a neutral partial (the combine skips M = -inf)
+    for (int r = tid; r < QR; r += C::THREADS) {
+      ws_ml[r * 2] = -INFINITY;
+      ws_ml[r * 2 + 1] = 0.f;
+    }
+    return;
+  }
+  if (tid == 0) {
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    for (int s = 0; s < C::NST; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int mi = 0; mi < MT2; mi++) {
+      mbar_init(&s_full[mi], 1);
+      mbar_init(&p_full[mi], 256);
+      mbar_init(&pv_done[mi], 1);
+    }
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  const int n_rows = rows->n_rows;
+  for (int idx = tid; idx < a.npad * a.ancw; idx += C::THREADS) {
+    const int m = idx / a.ancw, w = idx % a.ancw;
+    const int s = (m < n_rows) ? rows->sidx[m] : -1;
+    sAnc[idx] = (s >= 0) ? a.anc[(size_t)s * a.ancw + w] : 0u;
+  }
+  if (warp == 1) {   // keys below every live row's context limit need no tree mask
+    int cm = 0x7fffffff;
+    for (int m = lane; m < n_rows; m += 32) cm = min(cm, rows->ctx_lim[m]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cm = min(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+    if (lane == 0) *sCtxMin = cm;
+  }
+  __syncwarp();
+  if (warp == 0) tmem_alloc(tmem_holder, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  // dependents may launch only now: this CTA already holds its TMEM columns
+  pdl_trigger();
+  pdl_wait();   // Q and this tick's K/V rows come from the QKV GEMM
+  // Q tile (GQA-packed rows r = g * npad + m) into the K-major SW128 layout
+  for (int idx = tid; idx < QR * 16; idx += C::THREADS) {
+    const int r = idx >> 4, c16 = idx & 15;
+    const int g = r / a.npad, m = r % a.npad;
+    const int mi = r >> 7, rr = r & 127, b = c16 >> 3, c = c16 & 7;
+    uint8_t* dst = sQ + mi * 2 * TCA_BOX + b * TCA_BOX + rr * 128 + ((c ^ (rr & 7)) << 4);
+    cp_async16(dst, a.q + ((size_t)m * a.H + kvh * G + g) * ATT_HD + c16 * 8);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  fence_proxy_async_smem();
+  __syncthreads();
+  TCA_PROBE(1);
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer: pass 1 K tiles, pass 2 K + V tiles
+      const uint64_t pol = l2_evict_last_policy();
+      int st = 0;
+      uint32_t ph = 0;
+      for (int j = 0; j < 2 * T; j++) {
+        const bool pass2 = j >= T;
+        const int t = pass2 ? j - T : j;
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], (pass2 ? 4 : 2) * TCA_BOX);
+        uint8_t* sK = sKV + st * C::STAGE_BYTES;
+        const int y = kvh * a.max_ctx + kbeg + t * TCA_KT;
+        tma_load_2d(sK, &tmK, &full[st], 0, y, pol);
+        tma_load_2d(sK + TCA_BOX, &tmK, &full[st], 64, y, pol);
+        if (pass2) {
+          tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[st], 0, y, pol);
+          tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[st], 64, y, pol);
+        }
+        if (++st == C::NST) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      // Ping-pong over the two M-tiles: after P V of (step j, tile mi) comes
+      // Q K^T of (step j+1, tile mi), so one tile's softmax overlaps the other
+      // tile's MMAs.  Steps j < T are pass 1 (Q K^T only), j >= T pass 2.
+      constexpr uint32_t idesc_qk = umma_idesc_bf16(128, 128);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);   // B (V) MN-major
+      const uint32_t q0 = smem_u32(sQ);
+      const uint32_t kv0 = smem_u32(sKV);
+      auto stage_of = [&](int j) { return j % C::NST; };
+      auto issue_qk = [&](int j, int mi) {
+        if (mi == 0) mbar_wait(&full[stage_of(j)], (uint32_t)((j / C::NST) & 1));
+        // the S / P columns of tile mi must be free
+        if (j > 0) {
+          if (j - 1 < T) mbar_wait(&p_full[mi], (uint32_t)((j - 1) & 1));   // softmax read S
+          else mbar_wait(&pv_done[mi], (uint32_t)((j - 1 - T) & 1));        // P V read P
+        }
+        tc_fence_after();
+        const uint32_t k0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES);
+        const uint32_t tS = tmem + (uint32_t)(mi * 256);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk++) {
+          const uint32_t off = (uint32_t)((kk >> 2) * TCA_BOX + (kk & 3) * 32);
+          umma_bf16(tS, umma_sdesc_sw128(q0 + mi * 2 * TCA_BOX + off), umma_sdesc_sw128(k0 + off), idesc_qk,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[mi]);
+      };
+      auto issue_pv = [&](int j, int mi) {
+        mbar_wait(&p_full[mi], (uint32_t)(j & 1));   // P of this step written
+        tc_fence_after();
+        const uint32_t v0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES) + 2 * TCA_BOX;
+        const uint32_t tS = tmem + (uint32_t)(mi * 256), tO = tS + 128;
+        const int t = j - T;
+#pragma unroll
+        for (int ks = 0; ks < 8; ks++) {
+          const uint64_t bd = umma_sdesc_sw128_mn(v0 + ks * 2048, TCA_BOX, 1024);
+          // keys 16ks.. live in the column half ks / 4: P_hi at +0, P_lo at +32
+          const uint32_t pa = tS + (uint32_t)((ks >> 2) * 64 + (ks & 3) * 8);
+          umma_bf16_tmemA(tO, pa, bd, idesc_pv, (t > 0 || ks > 0) ? 1u : 0u);
+          if constexpr (PLO) umma_bf16_tmemA(tO, pa + 32, bd, idesc_pv, 1u);
+        }
+        umma_commit(&pv_done[mi]);
+      };
+      for (int mi = 0; mi < MT2; mi++) issue_qk(0, mi);
+      for (int j = 0; j < 2 * T; j++) {
+        for (int mi = 0; mi < MT2; mi++) {
+          if (j >= T) issue_pv(j, mi);
+          if (j + 1 < 2 * T) issue_qk(j + 1, mi);
+        }
+        umma_commit(&empty[stage_of(j)]);   // stage j's K / V reads are all issued
+      }
+      umma_commit(o_full);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax: two threads per query row (TMEM lane quarter
+    // warp % 4, key / column half hh); each writes P only into its own half
+    const int wi = warp - 2, mi = wi >> 3, q = warp & 3, hh = (wi >> 2) & 1;
+    const int rr = q * 32 + lane, r = mi * 128 + rr;
+    const int m = r % a.npad;
+    const bool live = m < n_rows;
+    const int ctxr = live ? rows->ctx_lim[m] : 0;
+    const int slr = live ? rows->sidx[m] : -1;
+    const int l_glo = rows->l_glo;
+    const int ctx_min = *sCtxMin;
+    const uint32_t tS = tmem + (uint32_t)(mi * 256) + ((uint32_t)(q * 32) << 16) + (uint32_t)(hh * 64);
+    float M = -INFINITY, L = 0.f;
+    for (int j = 0; j < 2 * T; j++) {
+      const bool pass2 = j >= T;
+      const int t = pass2 ? j - T : j;
+      if (j == T) {   // pass boundary: row max of both halves
+        if (hh == 1) sHalf[r] = M;
+        named_bar_sync(1 + mi, 256);
+        if (hh == 0) M = fmaxf(M, sHalf[r]);
+        named_bar_sync(1 + mi, 256);
+        if (hh == 0) sHalf[r] = M;
+        named_bar_sync(1 + mi, 256);
+        if (hh == 1) M = sHalf[r];
+      }
+      mbar_wait(&s_full[mi], j & 1);
+      tc_fence_after();
+      if (j == 0) TCA_PROBE(2);
+      if (j == T) TCA_PROBE(4);
+      if (j == 2 * T - 1) TCA_PROBE(6);
+      float s[64];
+#pragma unroll
+      for (int c = 0; c < 4; c++) tmem_ld16_nw(tS + c * 16, reinterpret_cast<uint32_t*>(s + c * 16));
+      tmem_ld_wait();
+      if (!pass2) {   // S is in registers: the next Q K^T may overwrite it
+        tc_fence_before();
+        mbar_arrive(&p_full[mi]);
+      }
+      const int key0 = kbeg + t * TCA_KT + hh * 64;
+      // raw scores; invisible keys -> -inf (ex2 maps them to 0 below)
+      if (!(key0 + 64 <= min(kend, ctx_min))) {
+#pragma unroll
+        for (int i = 0; i < 64; i++) {
+          const int key = key0 + i;
+          bool vis = live && key < kend;
+          if (vis && key >= ctxr) {
+            const int aa = key - l_glo;
+            vis = slr >= 0 && aa >= 0 && aa < a.max_live &&
+                  ((sAnc[m * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+          }
+          if (!vis) s[i] = -INFINITY;
+        }
+      }
+      if (!pass2) {
+        float mx[4] = {M, -INFINITY, -INFINITY, -INFINITY};   // independent chains
+#pragma unroll
+        for (int i = 0; i < 64; i++) mx[i & 3] = fmaxf(mx[i & 3], s[i]);
+        M = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        if (j == T - 1) TCA_PROBE(3);
+      } else {
+        // p = 2^(s * scale - M * scale): one FFMA + ex2 per element (the scale
+        // is positive, so the raw-score max is the scaled max); a row with no
+        // visible key has M = -inf and keeps p = 0
+        const float sc = a.scale_log2;
+        const float nm = (M == -INFINITY) ? 0.f : -M * sc;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; i++) {
+          const float p = ex2_approx(fmaf(s[i], sc, nm));
+          s[i] = p;
+          ls[i & 3] += p;
+        }
+        L += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        // P_hi -> this half's columns [0, 32); P_lo = p - float(P_hi) -> [32, 64)
+        // (hi halves unpacked with integer ops, no second rounding)
+        uint32_t pk[32], pl[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+          const float x0 = s[2 * i], x1 = s[2 * i + 1];
+          const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(&hb);
+          pk[i] = u;
+          if constexpr (PLO)
+            pl[i] = pack_bf16(x0 - __uint_as_float(u << 16), x1 - __uint_as_float(u & 0xFFFF0000u));
+        }
+        tmem_st32(tS, pk);
+        if constexpr (PLO) tmem_st32(tS + 32, pl);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[mi]);
+        if (j == T) TCA_PROBE(5);
+      }
+    }
+    // ---------------- unnormalised O half-row and (M, l) of this split
+    TCA_PROBE(7);
+    if (hh == 1) sHalf[r] = L;
+    named_bar_sync(1 + mi, 256);
+    if (hh == 0) L += sHalf[r];
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    TCA_PROBE(8);
+    float o[64];
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+      tmem_ld16_nw(tS - (uint32_t)(hh * 64) + 128 + (uint32_t)(hh * 64) + c * 16, reinterpret_cast<uint32_t*>(o + c * 16));
+    tmem_ld_wait();
+    // every MMA has completed: the Q / K / V buffers stage the warp's 32 half
+    // rows so that the workspace write is coalesced (a warp's rows r are
+    // consecutive); rows padded to 68 floats keep the 16-byte stores at 4 wavefronts
+    constexpr int SLD = 64 + 4;
+    float* stg = reinterpret_cast<float*>(smem) + (size_t)wi * 32 * SLD;
+#pragma unroll
+    for (int i = 0; i < 16; i++)
+      *reinterpret_cast<float4*>(stg + lane * SLD + 4 * i) = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    __syncwarp();
+    float* dst = ws_o + (size_t)(r - lane) * ATT_HD + hh * 64;
+#pragma unroll 8
+    for (int i = 0; i < 16; i++) {   // 32 rows x 16 float4: lane -> (row 2i + lane/16, chunk lane%16)
+      const int row = 2 * i + (lane >> 4), ch = lane & 15;
+      *reinterpret_cast<float4*>(dst + (size_t)row * ATT_HD + 4 * ch) =
+          *reinterpret_cast<const float4*>(stg + row * SLD + 4 * ch);
+    }
+    if (hh == 0) {
+      ws_ml[r * 2] = (M == -INFINITY) ? -INFINITY : M * a.scale_log2;   // log2 units, as the combine expects
+      ws_ml[r * 2 + 1] = L;
+    }
+    TCA_PROBE(9);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+}  // namespace fs

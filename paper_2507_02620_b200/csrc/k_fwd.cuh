@@ -393,10 +393,10 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
 
 // merge the split partials: o = sum_c O_c 2^(m_c - M) / sum_c l_c 2^(m_c - M)
 // grid (npad, H), block 128 (one thread per head-dim element)
-__global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks) {
+__global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks, int n_parts_fixed = 0) {
   const int m = blockIdx.x, h = blockIdx.y;
   if (m >= a.rows->n_rows) return;
-  const int n_parts = (a.rows->n_keys + ATT_KC - 1) / ATT_KC * ks;
+  const int n_parts = n_parts_fixed > 0 ? n_parts_fixed : (a.rows->n_keys + ATT_KC - 1) / ATT_KC * ks;
   const int G = a.H / a.Hkv;
   const int kvh = h / G, g = h % G;
   const int QR = G * a.npad;
