@@ -133,6 +133,9 @@ struct fs_ctx {
   int32_t* h_node = nullptr;
   // schedule (replicated on every rank)
   int l_glo = 0, x_new = -1, live = 0, n_live = 0, next_id = 0, seg_counter = 0;
+  // the accept walk (a12) enqueued by verify_step right after the commit; its
+  // record in h_rec is valid until the tree changes (submit / prune / prefix)
+  bool acc_ready = false;
   std::deque<Seg> queue;
   Seg slot[FS_MAX_STAGES];
   int n_cached[FS_MAX_STAGES] = {0};
@@ -1110,6 +1113,7 @@ int fs_set_logits_buffer(fs_ctx* c, float* dev_logits, int32_t rows_cap) {
 }
 
 static void reset_round(fs_ctx* c) {
+  c->acc_ready = false;
   c->live = 0;
   c->n_live = 0;
   c->next_id = 0;
@@ -1216,6 +1220,7 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
       L_top < 0)
     return fail(c, FS_EINVAL, "bad submit arguments");
   const bool nr = flags == FS_NEW_ROUND;
+  c->acc_ready = false;
   if (nr && c->live) return fail(c, FS_ESTATE, "round live");
   if (!nr && !c->live) return fail(c, FS_ESTATE, "no live round");
   const int base = nr ? 0 : c->next_id;
@@ -1315,6 +1320,14 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     CK_LAUNCH(c);
     CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * n, cudaMemcpyDeviceToHost, c->st));
     CK_CUDA(c, cudaMemcpyAsync(c->h_node, c->out_node, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+    // the accept walk (fs_accept) over the updated tree, under the same sync
+    c->acc_ready = false;
+    if (c->live && c->n_live > 0) {
+      accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
+      CK_LAUNCH(c);
+      CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+      c->acc_ready = true;
+    }
     if ((rc = sync(c))) return rc;
     if (out)
       for (int m = 0; m < n; m++) {
@@ -1339,10 +1352,13 @@ int fs_accept(fs_ctx* c, fs_accept_out* out) {
     out->progress = 0;
     return FS_OK;
   }
-  accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
-  CK_LAUNCH(c);
-  CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
-  if ((rc = sync(c))) return rc;
+  if (!c->acc_ready) {
+    accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
+    CK_LAUNCH(c);
+    CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+    if ((rc = sync(c))) return rc;
+  }
+  c->acc_ready = false;
   const TreeRecord* r = c->h_rec;
   out->progress = r->progress;
   if (!r->progress) return FS_OK;
@@ -1363,6 +1379,7 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
   if (!dcs) return fail(c, FS_EINVAL, "null decision");
   if (!c->live) return fail(c, FS_ESTATE, "no live round");
   if (!dcs->progress || dcs->n_acc < 1 || dcs->n_acc > c->n_live) return fail(c, FS_ESTATE, "no progress");
+  c->acc_ready = false;
   DecisionIn* di = c->h_dec;
   di->n_acc = dcs->n_acc;
   di->n_new_id = dcs->cont ? dcs->n_new : -1;
@@ -1436,7 +1453,8 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
     c->x_new = dcs->x_new;
     reset_round(c);
   }
-  if ((rc = sync(c))) return rc;
+  // no sync: the compaction kernels are stream-ordered before any later call,
+  // and no host buffer they touch is reused before the next sync
   return FS_OK;
 }
 
