@@ -352,7 +352,7 @@ def ours(args):
     if P == 1 and not args.no_cpu_baseline:
         rec["cpu_baseline"] = cpu_baseline(shape, trees[0], prefix, ranks, tokens / K, ticks / K,
                                            n_samples=1)
-    print(json.dumps(rec), flush=True)
+    emit(rec)
     gp.close()
 
 
@@ -429,7 +429,7 @@ def reference(args):
             secs.append(dt)
     tot = sum(secs)
     value = tok_per_pass * len(secs) / tot
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": "accepted tokens/s (pipelined tree verify)",
         "value": round(value, 5), "unit": "tok/s", "n_gpus": P, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(secs), 1),
@@ -442,10 +442,34 @@ def reference(args):
                                    f"{tok_per_pass:.2f} accepted tokens per pass as in the round"},
         "e2e": {"value": round(value, 5), "unit": "tok/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
+
+
+_JSON_OUT = None
+
+
+def emit(rec):
+    """The one JSON line of the contract, on the process's original stdout
+    (everything else -- including C-level prints such as NCCL's version banner
+    -- goes to stderr)."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(rec) + "\n")
+    out.flush()
+
+
+def _route_stdout_to_stderr():
+    global _JSON_OUT
+    try:
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        _JSON_OUT = os.fdopen(saved, "w")
+    except OSError:
+        _JSON_OUT = None
 
 
 if __name__ == "__main__":
+    _route_stdout_to_stderr()
     args = parse()
     if args.impl == "reference":
         reference(args)
