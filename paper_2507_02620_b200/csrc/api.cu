@@ -780,7 +780,7 @@ int layer_forward(fs_ctx* c, int l) {
     e.q_out = (bf16*)c->q;
     e.k_cache = (bf16*)kv_plane(c, l, 0);
     e.v_cache = (bf16*)kv_plane(c, l, 1);
-    e.kv_prefetch = getenv("FS_NO_KV_PF") ? 0 : 1;
+    e.kv_prefetch = getenv("FS_KV_PF") ? 1 : 0;   // measured: no gain, opt-in
     // L2 prefetch of the next GEMM's leading weights (keeps HBM busy across
     // epilogues, transitions and attention); budgets in MB, env-tunable
     if ((rc = launch_gemm(c, w.qkv, e, &w.o, pf_budget("FS_PF_QKV", c->pf_mb[0])))) return rc;
