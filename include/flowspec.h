@@ -107,6 +107,11 @@ int fs_set_prefix(fs_ctx* ctx, const int32_t* tok, int32_t n, int32_t mode,
 
 #define FS_NEW_ROUND 1 /* draft initialization step */
 #define FS_APPEND 2    /* expansion: S <- S || S_app */
+/* OR-ed into flags: order the batch breadth-first (depth asc, id asc) instead
+ * of by cumulative score -- the "FlowSpec w/o Score-Based Draft" ablation
+ * (Table 2; SPEC S:506 reading).
+ * Still topological, so every prefix stays ancestor-closed. */
+#define FS_ORDER_BFS 4
 typedef struct fs_submit_out {
   int32_t n;                     /* nodes added (after optional top-L) */
   int32_t s_base;                /* S index of the first added node */

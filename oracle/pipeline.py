@@ -134,7 +134,7 @@ class OraclePipeline:
         return toks
 
     # ------------------------------------------------------------ submit
-    def submit(self, new_round, parent_ids, tokens, own, l_max, l_top=0):
+    def submit(self, new_round, parent_ids, tokens, own, l_max, l_top=0, order_mode="score"):
         """Draft initialization or expansion append.
 
         NEW_ROUND: node 0 is the root (parent -1, token = x_new); ids 0..n-1.
@@ -187,7 +187,20 @@ class OraclePipeline:
                 cu[i] = np.float32(cu[p - base_id] * own[i])
             else:
                 cu[i] = np.float32(cur_cu[self.id2s[p]] * own[i])
-        order = T.score_order(cu, ids)
+        if order_mode == "bfs":   # ablation: breadth-first instead of score order
+            cur_depth = T.depth_of(self.par) if self.node else []
+            dep = [0] * n
+            for i in range(n):
+                p = parent_ids[i]
+                if new_round and i == 0:
+                    dep[i] = 0
+                elif p >= base_id:
+                    dep[i] = dep[p - base_id] + 1
+                else:
+                    dep[i] = cur_depth[self.id2s[p]] + 1
+            order = T.bfs_order(dep, ids)
+        else:
+            order = T.score_order(cu, ids)
         if l_top:
             order = T.top_L(order, l_top)
             keep = set(order)

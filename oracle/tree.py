@@ -31,6 +31,15 @@ def score_order(cu, ids):
     return sorted(range(len(cu)), key=lambda i: (-float(cu[i]), int(ids[i])))
 
 
+def bfs_order(depth, ids):
+    """Breadth-first (layer) order: the "FlowSpec w/o Score-Based Draft"
+    ablation (Table 2).  The paper does
+    not name the replacement order; BFS is the reading SPEC S:506 takes.  Depth
+    ascending, ties by node id ascending; topological because a parent is one
+    layer shallower.  Returns positions into depth/ids."""
+    return sorted(range(len(depth)), key=lambda i: (int(depth[i]), int(ids[i])))
+
+
 def top_L(order, L):
     """Top-L refinement: keep the L highest-scoring nodes."""
     return list(order[:L])

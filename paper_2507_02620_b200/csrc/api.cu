@@ -1215,11 +1215,12 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   int rc;
   if (!check(c, &rc)) return rc;
   if (!c->prefixed) return fail(c, FS_ESTATE, "no prefix");
-  if (flags != FS_NEW_ROUND && flags != FS_APPEND) return fail(c, FS_EINVAL, "bad flags");
+  const int32_t kind = flags & ~FS_ORDER_BFS;
+  if (kind != FS_NEW_ROUND && kind != FS_APPEND) return fail(c, FS_EINVAL, "bad flags");
   if (!parent || !token || !own || n < 1 || n > FS_MAX_LIVE || L_max < 1 || L_max > c->cfg.max_seg ||
       L_top < 0)
     return fail(c, FS_EINVAL, "bad submit arguments");
-  const bool nr = flags == FS_NEW_ROUND;
+  const bool nr = kind == FS_NEW_ROUND;
   c->acc_ready = false;
   if (nr && c->live) return fail(c, FS_ESTATE, "round live");
   if (!nr && !c->live) return fail(c, FS_ESTATE, "no live round");

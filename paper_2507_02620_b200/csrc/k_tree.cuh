@@ -140,12 +140,20 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
     }
     if (!__syncthreads_or(ready)) break;
   }
-  // score order: rank by count over (cu desc, id asc) (R10)
+  // score order: rank by count over (cu desc, id asc) (R10); or the
+  // breadth-first ablation order (FS_ORDER_BFS: depth asc, id asc)
   int rank = 0;
   if (i < n) {
-    for (int j = 0; j < n; j++) {
-      float cj = s_cu[j];
-      rank += (cj > cu) || (cj == cu && j < i);
+    if (in->flags & FS_ORDER_BFS) {
+      for (int j = 0; j < n; j++) {
+        const int dj = s_depth[j];
+        rank += (dj < depth) || (dj == depth && j < i);
+      }
+    } else {
+      for (int j = 0; j < n; j++) {
+        float cj = s_cu[j];
+        rank += (cj > cu) || (cj == cu && j < i);
+      }
     }
     s_rank[i] = rank;
   }

@@ -18,6 +18,7 @@ FS_OK, FS_EINVAL, FS_ENOMEM, FS_ESTATE, FS_ECAPACITY, FS_ECUDA, FS_ENCCL, FS_EPO
 FS_MAX_LIVE, FS_MAX_SEG, FS_MAX_STAGES = 512, 64, 8
 FS_PREFILL, FS_SYNTH_KV = 0, 1
 FS_NEW_ROUND, FS_APPEND = 1, 2
+FS_ORDER_BFS = 4   # OR into submit flags: breadth-first order (w/o-SBD ablation)
 FS_Q_STATE, FS_Q_NODE, FS_Q_TOKEN, FS_Q_PARENT, FS_Q_POS, FS_Q_ANC, FS_Q_CU, FS_Q_RETAIN = range(8)
 
 i32 = C.c_int32

@@ -65,17 +65,19 @@ def compare_tree(gp, op, ancw, where=""):
 
 
 def run_lockstep(gp, op, trees_fn, n_rounds, l_max, tol, check_tree=True, check_kv=None,
-                 append_fn=None, max_ticks=10000):
-    """trees_fn(round, op) -> tree dict (parent, token, own); both sides get it."""
+                 append_fn=None, max_ticks=10000, bfs=False):
+    """trees_fn(round, op) -> tree dict (parent, token, own); both sides get it.
+    bfs: breadth-first submit order (the w/o-SBD ablation, FS_ORDER_BFS)."""
     stats = Stats()
     ancw = gp.cfg.max_live // 32
     for r in range(n_rounds):
         t = trees_fn(r, op)
-        so = op.submit(True, t["parent"], t["token"], t["own"], l_max=l_max)
-        sg = gp.fs_submit_segment(1, t["parent"], t["token"], t["own"], l_max)
+        so = op.submit(True, t["parent"], t["token"], t["own"], l_max=l_max,
+                       order_mode="bfs" if bfs else "score")
+        sg = gp.fs_submit_segment(1 | (4 if bfs else 0), t["parent"], t["token"], t["own"], l_max)
         assert sg["order"] == so["order"], ("order", r)
         assert sg["bounds"] == [tuple(b) for b in so["bounds"]], ("bounds", r)
-        if "order" in t:
+        if "order" in t and not bfs:
             assert so["order"] == list(t["order"]), "generator target order not met"
         if check_tree:
             compare_tree(gp, op, ancw, f"submit r{r}")

@@ -119,6 +119,19 @@ def _append_batch(op, rng, n_new, vocab):
     return parent, token, own
 
 
+def test_tiny_bfs_order_lockstep_and_strategy_independence():
+    """f1 ablation: breadth-first submit order (FS_ORDER_BFS) is bit-exact with the
+    oracle, and commits the same greedy stream as score order (SPEC strategy
+    independence; R-def-2)."""
+    F, shape, gp, op, xo, xg = _pair("tiny")
+    st_b = run_lockstep(gp, op, planted_trees(shape, 15, 4, (0, 1, 2, 9), SEED), n_rounds=4,
+                        l_max=5, tol=1e-4, bfs=True)
+    F, shape, gp, op, xo, xg = _pair("tiny")
+    st_s = run_lockstep(gp, op, planted_trees(shape, 15, 4, (0, 1, 2, 9), SEED), n_rounds=4,
+                        l_max=5, tol=1e-4)
+    assert st_b.committed == st_s.committed and len(st_s.committed) == 16
+
+
 @pytest.mark.parametrize("name,P_l", [("tiny", 4), ("small", 8)])
 def test_lockstep_with_appended_batches(name, P_l):
     """Expansion input (a16): after every progress-free tick or mid-round prune

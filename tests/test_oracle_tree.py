@@ -202,3 +202,36 @@ def test_prune_equals_path_prefix_bruteforce(seed):
     # at l_glo..l_glo'-1 after compaction, SURVEY §8(c) "Compaction")
     if i_pr:
         assert max(i_acc) < min(i_pr)
+
+
+# ------------------------------------------------------------------ BFS ablation order (f1)
+def _levels_by_children(parent):
+    """Independent construction: level sets by walking parent -> children from
+    the roots, each level emitted in id order."""
+    kids = {}
+    for i, p in enumerate(parent):
+        kids.setdefault(p, []).append(i)
+    out, level = [], sorted(kids.get(-1, []))
+    while level:
+        out += level
+        level = sorted(c for v in level for c in kids.get(v, []))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_bfs_order_is_layer_order(seed):
+    t = gen.random_tree(seed, 48, 7, 50, 3)
+    par = t["parent"]
+    order = T.bfs_order(T.depth_of(par), list(range(len(par))))
+    assert order == _levels_by_children(par)
+    pos = {v: k for k, v in enumerate(order)}
+    for i, p in enumerate(par):   # topological: every prefix is ancestor-closed
+        if p >= 0:
+            assert pos[p] < pos[i]
+
+
+def test_bfs_equals_score_order_on_a_chain():
+    par = [-1, 0, 1, 2, 3]
+    cu = T.cumulative_scores(par, [1.0, 0.9, 0.8, 0.7, 0.6])
+    ids = list(range(5))
+    assert T.bfs_order(T.depth_of(par), ids) == T.score_order(cu, ids) == ids
