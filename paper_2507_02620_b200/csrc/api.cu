@@ -100,7 +100,7 @@ struct fs_ctx {
   float *x = nullptr, *hin = nullptr, *yf = nullptr;
   void *y = nullptr, *q = nullptr, *att = nullptr, *act = nullptr;
   float *gws = nullptr;
-  float* ssq = nullptr;   // [d/128][npad] per-tile sums of squares of the residual
+  float* ssq = nullptr;   // [d/32][npad] per-32-column sums of squares of the residual
   int* gcnt = nullptr;
   Top2* head_part = nullptr;
   RowResult* res = nullptr;
@@ -348,7 +348,7 @@ size_t carve(fs_ctx* c, char* base) {
   c->gws_floats = wsf;
   c->gws = c->bf ? cv.take<float>(wsf) : nullptr;
   c->gcnt = cv.take<int>(max_tiles);
-  c->ssq = cv.take<float>((size_t)((d + 127) / 128) * np);
+  c->ssq = cv.take<float>((size_t)((d + 127) / 128) * 4 * np);
   c->head_part = cv.take<Top2>((size_t)((V + 127) / 128) * np);
   c->res = cv.take<RowResult>(FS_MAX_SEG);
   c->out_node = cv.take<int32_t>(FS_MAX_SEG);
@@ -596,7 +596,7 @@ GemmEpi base_epi(fs_ctx* c) {
 GemmEpi norm_input(fs_ctx* c) {
   GemmEpi e = base_epi(c);
   e.scale_ssq = c->ssq;
-  e.scale_n = c->cfg.d_model / 128;
+  e.scale_n = c->cfg.d_model / 32;   // one partial per 32 residual columns (an epilogue warp's rows)
   e.eps = (float)c->cfg.rms_eps;
   return e;
 }
@@ -1632,6 +1632,17 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
         fprintf(stderr, "      aprobe %2d: min %8.2f p10 %8.2f med %8.2f p90 %8.2f max %8.2f (n=%zu)\n", k,
                 vals[0], vals[vals.size() / 10], vals[vals.size() / 2], vals[vals.size() * 9 / 10],
                 vals.back(), vals.size());
+      }
+    }
+    // raw per-CTA probe deltas (ns) of the last launch: timer granularity check
+    {
+      const size_t i = std::min(c->tl_names.size(), nl) - 1;
+      for (size_t cta = 0; cta < 4; cta++) {
+        const unsigned long long* pr = &h[i * per + cta * 16];
+        fprintf(stderr, "cta %zu raw deltas ns:", cta);
+        for (int k = 1; k < 15; k++)
+          if (pr[k] && pr[0]) fprintf(stderr, " %d:%lld", k, (long long)(pr[k] - pr[0]));
+        fprintf(stderr, "\n");
       }
     }
     c->tl_names.clear();

@@ -33,11 +33,11 @@ __global__ void norm_prep_kernel(const float* __restrict__ x, const bf16* __rest
     z[(size_t)m * d + k] = hi;
     z[(size_t)(np + m) * d + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
   }
-  for (int t = threadIdx.x; t < d / 128; t += blockDim.x) {
+  for (int t = threadIdx.x; t < d / 32; t += blockDim.x) {   // per-32-column partials
     float s = 0.f;
     if (live)
-      for (int k = 0; k < 128; k++) {
-        const float v = x[(size_t)m * d + t * 128 + k];
+      for (int k = 0; k < 32; k++) {
+        const float v = x[(size_t)m * d + t * 32 + k];
         s += v * v;
       }
     ssq[(size_t)t * np + m] = s;

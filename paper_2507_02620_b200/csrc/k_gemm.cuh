@@ -300,20 +300,44 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       }
     }
     if (threadIdx.x == 64 && sh.dbg) GEMM_PROBE(11);
-    if (ep.ssq_out) {  // deterministic per-tile sum of squares of the new residual rows
+    if (ep.ssq_out) {  // deterministic sums of squares of the new residual rows: one
+      // partial per warp (32 output columns); the consumer sums d / 32 of them
+      if constexpr (NT == 16) {
+        // reduce-scatter butterfly: every step keeps half of the columns and adds
+        // the partner lane's copy of them (16 shuffles for all 16 columns, no
+        // branches); lane ends with column ((l>>4)&1)*8 + ((l>>3)&1)*4 + ((l>>2)&1)*2 + ((l>>1)&1)
+        float w8[8], w4[4], w2[2];
+        const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
 #pragma unroll
-      for (int m = 0; m < NT; m++) {
-        if (m < mlo || m >= mhi) continue;
-        float z = sq[m];
+        for (int k = 0; k < 8; k++) {
+          const float send = u16 ? sq[k] : sq[k + 8];
+          w8[k] = (u16 ? sq[k + 8] : sq[k]) + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-        if (lane == 0) xch[q * NT + m] = z;
+        for (int k = 0; k < 4; k++) {
+          const float send = u8 ? w8[k] : w8[k + 4];
+          w4[k] = (u8 ? w8[k + 4] : w8[k]) + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+          const float send = u4 ? w4[k] : w4[k + 2];
+          w2[k] = (u4 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        const float send = u2 ? w2[0] : w2[1];
+        float z = (u2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+        z += __shfl_xor_sync(0xffffffffu, z, 1);
+        const int col = (u16 ? 8 : 0) + (u8 ? 4 : 0) + (u4 ? 2 : 0) + (u2 ? 1 : 0);
+        if (!(lane & 1) && col >= mlo && col < mhi) ep.ssq_out[((size_t)t * 4 + q) * NT + col] = z;
+      } else {
+#pragma unroll
+        for (int m = 0; m < NT; m++) {
+          if (m < mlo || m >= mhi) continue;
+          float z = sq[m];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+          if (lane == 0) ep.ssq_out[((size_t)t * 4 + q) * NT + m] = z;
+        }
       }
-      named_bar_sync(1, 128);
-      if (row >= mlo && row < mhi)
-        ep.ssq_out[(size_t)t * NT + row] =
-            ((xch[0 * NT + row] + xch[1 * NT + row]) + xch[2 * NT + row]) + xch[3 * NT + row];
-      named_bar_sync(1, 128);
     }
   } else if (ep.mode == EPI_HEAD) {
     const bool valid = ng < ep.vocab;
