@@ -445,6 +445,266 @@ FS_DEV float ex2_approx(float x) {
   return y;
 }
 
+// ---- MHA attention building blocks, shared by attn_mha_kernel and the fused
+// QKV + attention kernel (k_qkv_attn.cuh).  tid / warp / lane are the indices
+// within the 4 attention warps; bar_id names the barrier of those 128 threads.
+
+// per-warp running state of one m16 query tile over its key slice
+template <int KPW>
+struct MhaWarp {
+  float oacc[16][4];
+  float mrow[2], lrow[2];
+  uint32_t qf[ATT_HD / 16][4];
+  int qm[2], ctx[2], sl[2];
+  int mt, ks;
+};
+
+template <int KPW>
+FS_DEV void mha_warp_init(MhaWarp<KPW>& w, const AttnArgs& a, int warp, int lane, int n_rows) {
+  const int QR = (a.H / a.Hkv) * a.npad, MT = QR / 16;
+  w.mt = warp % MT;
+  w.ks = warp / MT;
+  const int g_row = lane >> 2;
+  for (int h2 = 0; h2 < 2; h2++) {
+    const int r = w.mt * 16 + g_row + 8 * h2;
+    w.qm[h2] = r % a.npad;
+    w.ctx[h2] = (w.qm[h2] < n_rows) ? a.rows->ctx_lim[w.qm[h2]] : 0;
+    w.sl[h2] = (w.qm[h2] < n_rows) ? a.rows->sidx[w.qm[h2]] : -1;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++) w.oacc[j][0] = w.oacc[j][1] = w.oacc[j][2] = w.oacc[j][3] = 0.f;
+  w.mrow[0] = w.mrow[1] = -INFINITY;
+  w.lrow[0] = w.lrow[1] = 0.f;
+}
+
+// Q fragments of the warp's m-tile into registers (once)
+template <int KPW>
+FS_DEV void mha_load_q(MhaWarp<KPW>& w, const bf16* sQ, int lane) {
+#pragma unroll
+  for (int kk = 0; kk < ATT_HD / 16; kk++)
+    ldsm_x4(w.qf[kk][0], w.qf[kk][1], w.qf[kk][2], w.qf[kk][3],
+            sQ + (size_t)(w.mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
+}
+
+// one 64-key sub-chunk (keys kbase..kbase+63 in sK / sV): the warp's KPW keys,
+// tree mask unless every key is context of every live row, online softmax, P V
+// with P as a bf16 hi/lo pair (R18)
+template <int KPW>
+FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, const bf16* sV, int kbase,
+                         int kend, int ctx_min, int l_glo, int n_rows, const uint32_t* sAnc, int lane) {
+  constexpr int NT8 = KPW / 8;
+  const int t4 = lane & 3;
+  const int kb = w.ks * KPW;
+  const int key0 = kbase + kb;
+  float sacc[NT8][4];
+#pragma unroll
+  for (int j = 0; j < NT8; j++) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < ATT_HD / 16; kk++) {
+#pragma unroll
+    for (int j = 0; j < NT8; j++) {
+      uint32_t b0, b1;
+      ldsm_x2(b0, b1, sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8);
+      mma_bf16_16816(sacc[j], w.qf[kk][0], w.qf[kk][1], w.qf[kk][2], w.qf[kk][3], b0, b1);
+    }
+  }
+  float mnew[2] = {w.mrow[0], w.mrow[1]};
+  if (key0 + KPW <= min(kend, ctx_min)) {
+    // every key of this warp is context of every live row: no tree mask
+    // (padding rows produce finite values that are never written)
+#pragma unroll
+    for (int j = 0; j < NT8; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const float v = sacc[j][e] * a.scale_log2;
+        sacc[j][e] = v;
+        mnew[e >> 1] = fmaxf(mnew[e >> 1], v);
+      }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NT8; j++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int h2 = e >> 1;
+        const int key = key0 + j * 8 + t4 * 2 + (e & 1);
+        bool vis = key < kend && w.qm[h2] < n_rows;
+        if (vis && key >= w.ctx[h2]) {
+          const int aa = key - l_glo;
+          vis = w.sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
+                ((sAnc[w.qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+        }
+        const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
+        sacc[j][e] = v;
+        mnew[h2] = fmaxf(mnew[h2], v);
+      }
+  }
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) {
+    mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 1));
+    mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 2));
+  }
+  float corr[2], rs[2] = {0.f, 0.f};
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) {
+    corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : ex2_approx(w.mrow[h2] - mnew[h2]);
+    w.mrow[h2] = mnew[h2];
+  }
+#pragma unroll
+  for (int j = 0; j < NT8; j++)
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int h2 = e >> 1;
+      const float p = (sacc[j][e] == -INFINITY) ? 0.f : ex2_approx(sacc[j][e] - w.mrow[h2]);
+      sacc[j][e] = p;
+      rs[h2] += p;
+    }
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) w.lrow[h2] = w.lrow[h2] * corr[h2] + rs[h2];
+#pragma unroll
+  for (int j = 0; j < 16; j++) {
+    w.oacc[j][0] *= corr[0];
+    w.oacc[j][1] *= corr[0];
+    w.oacc[j][2] *= corr[1];
+    w.oacc[j][3] *= corr[1];
+  }
+  // O += P V with P as a bf16 hi + lo pair (R18: fp32 softmax/accumulation)
+#pragma unroll
+  for (int kk = 0; kk < KPW / 16; kk++) {
+    uint32_t ph[4], pl[4];
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      const int jt = 2 * kk + (f >> 1), e0 = (f & 1) * 2;
+      const float x0 = sacc[jt][e0], x1 = sacc[jt][e0 + 1];
+      const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+      ph[f] = *reinterpret_cast<const uint32_t*>(&h);
+      pl[f] = pack_bf16(x0 - __bfloat162float(h.x), x1 - __bfloat162float(h.y));
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      uint32_t b0, b1;
+      ldsm_x2_t(b0, b1, sV + (size_t)(kb + kk * 16 + (lane & 15)) * ATT_LD + j * 8);
+      mma_bf16_16816(w.oacc[j], ph[0], ph[1], ph[2], ph[3], b0, b1);
+      mma_bf16_16816(w.oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
+    }
+  }
+}
+
+// merge the KS key-warps of each m-tile into the CTA partial sPart [QR][HD] +
+// sPml [QR][2] (scratch: `so` [4][16][SO_LD] + [4][16][2], which may alias the
+// K/V ring: every warp is past its last sub-chunk at the first barrier)
+template <int KPW>
+FS_DEV void mha_ks_merge(MhaWarp<KPW>& w, const AttnArgs& a, float* so, float* sPart, float* sPml, int tid,
+                         int warp, int lane, int bar_id) {
+  constexpr int KS = ATT_SUB / KPW;
+  const int QR = (a.H / a.Hkv) * a.npad, MT = QR / 16;
+  const int g_row = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int h2 = 0; h2 < 2; h2++) {
+    w.lrow[h2] += __shfl_xor_sync(0xffffffffu, w.lrow[h2], 1);
+    w.lrow[h2] += __shfl_xor_sync(0xffffffffu, w.lrow[h2], 2);
+  }
+  float* sml = so + 4 * 16 * ATT_SO_LD;                       // [4][16][2]
+  named_bar_sync(bar_id, 128);
+  for (int h2 = 0; h2 < 2; h2++) {
+    const int r16 = g_row + 8 * h2;
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+      *reinterpret_cast<float2*>(so + ((size_t)warp * 16 + r16) * ATT_SO_LD + j * 8 + t4 * 2) =
+          make_float2(w.oacc[j][2 * h2], w.oacc[j][2 * h2 + 1]);
+    if (t4 == 0) {
+      sml[(warp * 16 + r16) * 2] = w.mrow[h2];
+      sml[(warp * 16 + r16) * 2 + 1] = w.lrow[h2];
+    }
+  }
+  named_bar_sync(bar_id, 128);
+  // 8 threads per row, 16 head dims (4 x float4) each; KS <= 4 unrolled
+  for (int r = tid >> 3; r < QR; r += 16) {
+    const int m2 = r / 16, r16 = r % 16, d0 = (tid & 7) * 16;
+    float mm[KS], M = -INFINITY;
+#pragma unroll
+    for (int k2 = 0; k2 < KS; k2++) {
+      mm[k2] = sml[((m2 + MT * k2) * 16 + r16) * 2];
+      M = fmaxf(M, mm[k2]);
+    }
+    float L = 0.f;
+    float4 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k2 = 0; k2 < KS; k2++) {
+      const int ww = m2 + MT * k2;
+      const float wt = (mm[k2] == -INFINITY) ? 0.f : exp2f(mm[k2] - M);
+      L += sml[(ww * 16 + r16) * 2 + 1] * wt;
+      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)ww * 16 + r16) * ATT_SO_LD + d0);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const float4 o = src[u];
+        acc[u].x += o.x * wt;
+        acc[u].y += o.y * wt;
+        acc[u].z += o.z * wt;
+        acc[u].w += o.w * wt;
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(sPart + r * ATT_HD + d0);
+#pragma unroll
+    for (int u = 0; u < 4; u++) dst[u] = acc[u];
+    if ((tid & 7) == 0) {
+      sPml[r * 2] = M;
+      sPml[r * 2 + 1] = L;
+    }
+  }
+}
+
+// after a cluster barrier: CTA rank crank merges rows crank, crank + nsplit, ...
+// of all splits through distributed shared memory (split order: deterministic)
+// and writes the bf16 hi/lo attention output pair
+FS_DEV void mha_cluster_merge(const AttnArgs& a, bf16* out, const float* sPart, const float* sPml, int crank,
+                              int nsplit, int kvh, int n_rows, int tid) {
+  const int G = a.H / a.Hkv, QR = G * a.npad;
+  for (int rr = crank + nsplit * (tid >> 5); rr < QR; rr += nsplit * 4) {
+    const int m = rr % a.npad, g = rr / a.npad;
+    if (m >= n_rows) continue;
+    const int q4 = (tid & 31) * 4;
+    float mm[8], ll[8], M = -INFINITY;
+    float4 oo[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) {   // all ranks' loads in flight together
+      mm[c] = -INFINITY;
+      ll[c] = 0.f;
+      oo[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < nsplit) {
+        const uint32_t pm = dsmem_addr(sPml + rr * 2, (uint32_t)c);
+        mm[c] = ld_dsmem_f32(pm);
+        ll[c] = ld_dsmem_f32(pm + 4);
+        oo[c] = ld_dsmem_f32x4(dsmem_addr(sPart + rr * ATT_HD + q4, (uint32_t)c));
+      }
+      M = fmaxf(M, mm[c]);
+    }
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      if (c < nsplit && mm[c] != -INFINITY) {
+        const float wt = exp2f(mm[c] - M);
+        L += ll[c] * wt;
+        acc.x += oo[c].x * wt;
+        acc.y += oo[c].y * wt;
+        acc.z += oo[c].z * wt;
+        acc.w += oo[c].w * wt;
+      }
+    }
+    const float v[4] = {acc.x / L, acc.y / L, acc.z / L, acc.w / L};
+    const size_t base = ((size_t)m * a.H + kvh * G + g) * ATT_HD + q4;
+    const size_t lob = ((size_t)(a.npad + m) * a.H + kvh * G + g) * ATT_HD + q4;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const bf16 hi = __float2bfloat16_rn(v[u]);
+      out[base + u] = hi;
+      out[lob + u] = __float2bfloat16_rn(v[u] - __bfloat162float(hi));
+    }
+  }
+}
+
 template <int KPW>
 __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   namespace cg = cooperative_groups;
@@ -523,25 +783,10 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   while (issued < npre) load_sub(issued++);
   pdl_trigger();
   ATT_PROBE(1);
-  const int mt = warp % MT, ks = warp / MT;
-  const int g_row = lane >> 2, t4 = lane & 3;
-  int qm[2], ctx[2], sl[2];
-  for (int h2 = 0; h2 < 2; h2++) {
-    const int r = mt * 16 + g_row + 8 * h2;
-    qm[h2] = r % a.npad;
-    ctx[h2] = (qm[h2] < n_rows) ? rows->ctx_lim[qm[h2]] : 0;
-    sl[h2] = (qm[h2] < n_rows) ? rows->sidx[qm[h2]] : -1;
-  }
+  MhaWarp<KPW> w;
+  mha_warp_init<KPW>(w, a, warp, lane, n_rows);
   const int l_glo = rows->l_glo;
-  float oacc[16][4];
-#pragma unroll
-  for (int j = 0; j < 16; j++) oacc[j][0] = oacc[j][1] = oacc[j][2] = oacc[j][3] = 0.f;
-  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
-  constexpr int NT8 = KPW / 8;
-  uint32_t qf[ATT_HD / 16][4];
   int ctx_min = 0;
-  // groups committed so far: pre-dependency sub-chunks, Q, remaining prefetch;
-  // wait until sub-chunk sc and Q have landed
   for (int sc = 0; sc < nsc; sc++) {
     // cp.async groups in commit order: early sub-chunks, Q, later sub-chunks.
     // Both sub-chunk sc and Q must have landed: allow only the groups younger
@@ -555,228 +800,23 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     ATT_PROBE(2 + min(sc, 7));
     const bf16* sK = sKV + (size_t)(sc % ATT_NBUF) * 2 * ATT_SUB * ATT_LD;
     const bf16* sV = sK + ATT_SUB * ATT_LD;
-    const int kb = ks * KPW;
-    const int key0 = kbeg + sc * ATT_SUB + kb;
     if (sc == 0) {  // Q fragments of this m-tile stay in registers for every sub-chunk
-#pragma unroll
-      for (int kk = 0; kk < ATT_HD / 16; kk++)
-        ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3],
-                sQ + (size_t)(mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
+      mha_load_q<KPW>(w, sQ, lane);
       ctx_min = *sCtxMin;
     }
-    float sacc[NT8][4];
-#pragma unroll
-    for (int j = 0; j < NT8; j++) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < ATT_HD / 16; kk++) {
-#pragma unroll
-      for (int j = 0; j < NT8; j++) {
-        uint32_t b0, b1;
-        ldsm_x2(b0, b1, sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8);
-        mma_bf16_16816(sacc[j], qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], b0, b1);
-      }
-    }
-    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: QK^T done
-      if (sacc[0][0] == 12345.f) a.dbg[1] = 0;
-      ATT_PROBE(5);
-    }
-    float mnew[2] = {mrow[0], mrow[1]};
-    if (key0 + KPW <= min(kend, ctx_min)) {
-      // every key of this warp is context of every live row: no tree mask
-      // (padding rows produce finite values that are never written)
-#pragma unroll
-      for (int j = 0; j < NT8; j++)
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const float v = sacc[j][e] * a.scale_log2;
-          sacc[j][e] = v;
-          mnew[e >> 1] = fmaxf(mnew[e >> 1], v);
-        }
-    } else {
-#pragma unroll
-      for (int j = 0; j < NT8; j++)
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const int h2 = e >> 1;
-          const int key = key0 + j * 8 + t4 * 2 + (e & 1);
-          bool vis = key < kend && qm[h2] < n_rows;
-          if (vis && key >= ctx[h2]) {
-            const int aa = key - l_glo;
-            vis = sl[h2] >= 0 && aa >= 0 && aa < a.max_live &&
-                  ((sAnc[qm[h2] * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
-          }
-          const float v = vis ? sacc[j][e] * a.scale_log2 : -INFINITY;
-          sacc[j][e] = v;
-          mnew[h2] = fmaxf(mnew[h2], v);
-        }
-    }
-#pragma unroll
-    for (int h2 = 0; h2 < 2; h2++) {
-      mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 1));
-      mnew[h2] = fmaxf(mnew[h2], __shfl_xor_sync(0xffffffffu, mnew[h2], 2));
-    }
-    float corr[2], rs[2] = {0.f, 0.f};
-#pragma unroll
-    for (int h2 = 0; h2 < 2; h2++) {
-      corr[h2] = (mnew[h2] == -INFINITY) ? 1.f : ex2_approx(mrow[h2] - mnew[h2]);
-      mrow[h2] = mnew[h2];
-    }
-#pragma unroll
-    for (int j = 0; j < NT8; j++)
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int h2 = e >> 1;
-        const float p = (sacc[j][e] == -INFINITY) ? 0.f : ex2_approx(sacc[j][e] - mrow[h2]);
-        sacc[j][e] = p;
-        rs[h2] += p;
-      }
-#pragma unroll
-    for (int h2 = 0; h2 < 2; h2++) lrow[h2] = lrow[h2] * corr[h2] + rs[h2];
-#pragma unroll
-    for (int j = 0; j < 16; j++) {
-      oacc[j][0] *= corr[0];
-      oacc[j][1] *= corr[0];
-      oacc[j][2] *= corr[1];
-      oacc[j][3] *= corr[1];
-    }
-    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: softmax done
-      if (sacc[0][0] + oacc[15][3] == 12345.f) a.dbg[1] = 0;
-      ATT_PROBE(6);
-    }
-    // O += P V with P as a bf16 hi + lo pair (R18: fp32 softmax/accumulation)
-#pragma unroll
-    for (int kk = 0; kk < KPW / 16; kk++) {
-      uint32_t ph[4], pl[4];
-#pragma unroll
-      for (int f = 0; f < 4; f++) {
-        const int jt = 2 * kk + (f >> 1), e0 = (f & 1) * 2;
-        const float x0 = sacc[jt][e0], x1 = sacc[jt][e0 + 1];
-        const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-        ph[f] = *reinterpret_cast<const uint32_t*>(&h);
-        pl[f] = pack_bf16(x0 - __bfloat162float(h.x), x1 - __bfloat162float(h.y));
-      }
-#pragma unroll
-      for (int j = 0; j < 16; j++) {
-        uint32_t b0, b1;
-        ldsm_x2_t(b0, b1, sV + (size_t)(kb + kk * 16 + (lane & 15)) * ATT_LD + j * 8);
-        mma_bf16_16816(oacc[j], ph[0], ph[1], ph[2], ph[3], b0, b1);
-        mma_bf16_16816(oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
-      }
-    }
-    if (sc == 1 && a.dbg && threadIdx.x == 0) {   // diagnostics: PV done
-      if (oacc[0][0] + oacc[15][3] == 12345.f) a.dbg[1] = 0;
-      ATT_PROBE(7);
-    }
+    mha_subchunk<KPW>(w, a, sK, sV, kbeg + sc * ATT_SUB, kend, ctx_min, l_glo, n_rows, sAnc, lane);
     __syncthreads();                                    // ring slot sc free
-    if (sc == 1) ATT_PROBE(8);
     if (issued < nsc) load_sub(issued++);
-  }
-#pragma unroll
-  for (int h2 = 0; h2 < 2; h2++) {
-    lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 1);
-    lrow[h2] += __shfl_xor_sync(0xffffffffu, lrow[h2], 2);
   }
   ATT_PROBE(10);
   // ---- merge the KS key-warps of each m-tile (shared memory)
-  float* so = reinterpret_cast<float*>(sKV);                  // [4][16][SO_LD] (padded rows)
-  float* sml = so + 4 * 16 * ATT_SO_LD;                       // [4][16][2]
-  __syncthreads();
-  for (int h2 = 0; h2 < 2; h2++) {
-    const int r16 = g_row + 8 * h2;
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-      *reinterpret_cast<float2*>(so + ((size_t)warp * 16 + r16) * ATT_SO_LD + j * 8 + t4 * 2) =
-          make_float2(oacc[j][2 * h2], oacc[j][2 * h2 + 1]);
-    if (t4 == 0) {
-      sml[(warp * 16 + r16) * 2] = mrow[h2];
-      sml[(warp * 16 + r16) * 2 + 1] = lrow[h2];
-    }
-  }
-  __syncthreads();
-  // 8 threads per row, 16 head dims (4 x float4) each; KS <= 4 unrolled
-  for (int r = tid >> 3; r < QR; r += 16) {
-    const int m2 = r / 16, r16 = r % 16, d0 = (tid & 7) * 16;
-    float mm[KS], M = -INFINITY;
-#pragma unroll
-    for (int k2 = 0; k2 < KS; k2++) {
-      mm[k2] = sml[((m2 + MT * k2) * 16 + r16) * 2];
-      M = fmaxf(M, mm[k2]);
-    }
-    float L = 0.f;
-    float4 acc[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int k2 = 0; k2 < KS; k2++) {
-      const int w = m2 + MT * k2;
-      const float wt = (mm[k2] == -INFINITY) ? 0.f : exp2f(mm[k2] - M);
-      L += sml[(w * 16 + r16) * 2 + 1] * wt;
-      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)w * 16 + r16) * ATT_SO_LD + d0);
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const float4 o = src[u];
-        acc[u].x += o.x * wt;
-        acc[u].y += o.y * wt;
-        acc[u].z += o.z * wt;
-        acc[u].w += o.w * wt;
-      }
-    }
-    float4* dst = reinterpret_cast<float4*>(sPart + r * ATT_HD + d0);
-#pragma unroll
-    for (int u = 0; u < 4; u++) dst[u] = acc[u];
-    if ((tid & 7) == 0) {
-      sPml[r * 2] = M;
-      sPml[r * 2 + 1] = L;
-    }
-  }
+  mha_ks_merge<KPW>(w, a, reinterpret_cast<float*>(sKV), sPart, sPml, tid, warp, lane, 0);
   // ---- cluster merge of the splits through distributed shared memory:
   // CTA rank r owns rows r, r+nsplit, ...; 32 threads (float4 each) per row
   ATT_PROBE(11);
   cluster.sync();
   ATT_PROBE(12);
-  const int crank = (int)cluster.block_rank();
-  for (int rr = crank + nsplit * (tid >> 5); rr < QR; rr += nsplit * 4) {
-    const int m = rr % a.npad, g = rr / a.npad;
-    if (m >= n_rows) continue;
-    const int q4 = (tid & 31) * 4;
-    float mm[8], ll[8], M = -INFINITY;
-    float4 oo[8];
-#pragma unroll
-    for (int c = 0; c < 8; c++) {   // all ranks' loads in flight together
-      mm[c] = -INFINITY;
-      ll[c] = 0.f;
-      oo[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c < nsplit) {
-        const uint32_t pm = dsmem_addr(sPml + rr * 2, (uint32_t)c);
-        mm[c] = ld_dsmem_f32(pm);
-        ll[c] = ld_dsmem_f32(pm + 4);
-        oo[c] = ld_dsmem_f32x4(dsmem_addr(sPart + rr * ATT_HD + q4, (uint32_t)c));
-      }
-      M = fmaxf(M, mm[c]);
-    }
-    float L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int c = 0; c < 8; c++) {
-      if (c < nsplit && mm[c] != -INFINITY) {
-        const float wt = exp2f(mm[c] - M);
-        L += ll[c] * wt;
-        acc.x += oo[c].x * wt;
-        acc.y += oo[c].y * wt;
-        acc.z += oo[c].z * wt;
-        acc.w += oo[c].w * wt;
-      }
-    }
-    const float v[4] = {acc.x / L, acc.y / L, acc.z / L, acc.w / L};
-    const size_t base = ((size_t)m * a.H + kvh * G + g) * ATT_HD + q4;
-    const size_t lob = ((size_t)(a.npad + m) * a.H + kvh * G + g) * ATT_HD + q4;
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const bf16 hi = __float2bfloat16_rn(v[u]);
-      args.out[base + u] = hi;
-      args.out[lob + u] = __float2bfloat16_rn(v[u] - __bfloat162float(hi));
-    }
-  }
+  mha_cluster_merge(a, args.out, sPart, sPml, (int)cluster.block_rank(), nsplit, kvh, n_rows, tid);
   ATT_PROBE(13);
   // keep every CTA's shared memory alive until all DSMEM reads are done (they
   // were consumed before arriving): relaxed, the output stores need not drain
