@@ -19,7 +19,7 @@ import torch.distributed as dist
 from oracle.pipeline import OraclePipeline
 from paper_2507_02620_b200 import flowspec as F
 from synth import gen
-from synth.configs import SHAPES
+from synth.configs import SHAPES, reduced
 from tests.lockstep import planted_trees, run_lockstep
 
 SEED = 0x5EED01
@@ -27,6 +27,9 @@ SEED = 0x5EED01
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "tiny"
+    n_layers = None
+    if ":" in name:   # "shape:L" -> the same per-layer shapes with L layers
+        name, n_layers = name.split(":")[0], int(name.split(":")[1])
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -34,7 +37,7 @@ def main():
     dist.init_process_group("gloo")
     obj = [F.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    shape = SHAPES[name]
+    shape = SHAPES[name] if n_layers is None else reduced(name, n_layers)
     P = world
     lps = None
     gp = F.Pipeline(shape, n_stages=P, rank=rank, max_ctx=1024, max_seg=16, device=local,
