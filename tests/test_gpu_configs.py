@@ -14,7 +14,8 @@ pytestmark = pytest.mark.gpu
 SEED = 0x5EED01
 
 
-def _run(name, prefix_len, mode, max_seg, l_max, n_nodes, depth, planted, max_ctx, n_rounds):
+def _run(name, prefix_len, mode, max_seg, l_max, n_nodes, depth, planted, max_ctx, n_rounds,
+         append_batches=0):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -29,8 +30,27 @@ def _run(name, prefix_len, mode, max_seg, l_max, n_nodes, depth, planted, max_ct
     xg = gp.fs_set_prefix(prefix, F.FS_SYNTH_KV if mode == "synth" else F.FS_PREFILL, kv_seed=7)
     srt = np.sort(op.prefix_logits)
     assert xg == xo or srt[-1] - srt[-2] < 1e-2
+    append_fn = None
+    appended = [0]
+    if append_batches:
+        from tests.test_gpu_parity import _append_batch
+        rng = gen.Rng(91)
+
+        def append_fn(r, ticks, gp_, op_):
+            # steady expansion (configs[3], scenario S): a 16-node batch, its own
+            # segment (L_exp = -1), after every tick while the round is live
+            if not op_.live or appended[0] >= append_batches or len(op_.node) + 16 > 480:
+                return
+            parent, token, own = _append_batch(op_, rng, 16, shape.vocab)
+            so = op_.submit(False, parent, token, own, l_max=16)
+            sg = gp_.fs_submit_segment(F.FS_APPEND, parent, token, own, 16)
+            assert sg["order"] == so["order"] and sg["bounds"] == [tuple(b) for b in so["bounds"]]
+            appended[0] += 1
+
     st = run_lockstep(gp, op, planted_trees(shape, n_nodes, depth, planted, SEED), n_rounds=n_rounds,
-                      l_max=l_max, tol=2e-2)
+                      l_max=l_max, tol=2e-2, append_fn=append_fn)
+    if append_batches:
+        assert appended[0] > 0
     print(f"{name}: max|dlogit| {st.max_abs:.3e} rows {st.rows} flagged {st.flagged} "
           f"overrides {st.overrides} committed {len(st.committed)}")
     return st
@@ -39,6 +59,13 @@ def _run(name, prefix_len, mode, max_seg, l_max, n_nodes, depth, planted, max_ct
 def test_13b_layers_expansion_shapes():
     """configs[3] per-layer shapes (d 5120, 40 heads, ffn 13824), 16-row segments."""
     _run("13b_l2", 300, "synth", 16, 16, 64, 6, (0, 2, 5, 17, 21), 1024, 2)
+
+
+def test_13b_config4_long_context_steady_expansion():
+    """configs[3] scenario on the per-layer shapes: 4096-token synthetic-KV
+    context, 128-node initial trees, appended 16-node batches (own segments)
+    while the round is live."""
+    _run("13b_l2", 4096, "synth", 16, 16, 128, 6, (0, 2, 5, 17, 21, 40), 4800, 2, append_batches=6)
 
 
 def test_72b_layers_gqa_bias_32row_segments_long_context():
