@@ -74,6 +74,20 @@ def test_host_only_entry_points(fsmod):
     assert lib.fs_init(C.byref(cfg), None) == fsmod.FS_EINVAL
 
 
+def test_smoke_and_bench_configurations_are_accepted(fsmod):
+    """The configurations __graft_entry__.smoke() and bench.py construct pass the
+    library's validation (host-only check, no GPU needed)."""
+    lib = fsmod.lib()
+    smoke = fsmod.make_config(SHAPES["small"], max_ctx=1024, max_seg=16)
+    assert lib.fs_arena_bytes(C.byref(smoke)) > 0
+    for P in (1, 2, 4, 8):
+        cfg = fsmod.make_config(SHAPES["7b"], n_stages=P, rank=P - 1, max_ctx=1024 + 4 * 23 * 7 + 600,
+                                max_seg=16)
+        assert lib.fs_arena_bytes(C.byref(cfg)) > 0, P
+    # max_ctx must cover max_live draft slots beyond the context
+    assert lib.fs_arena_bytes(C.byref(fsmod.make_config(SHAPES["small"], max_ctx=256, max_seg=16))) == 0
+
+
 def test_no_oracle_in_product_path():
     pkg = os.path.join(ROOT, "paper_2507_02620_b200")
     for dirpath, _, files in os.walk(pkg):
