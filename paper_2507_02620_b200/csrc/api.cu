@@ -77,10 +77,6 @@ struct fs_ctx {
   int P = 1, rank = 0, L0 = 0, L1 = 0, nl = 0;
   bool first = true, last = true, bf = true;
   int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536, gemm_ctas = 2;
-  // L2 prefetch budgets (MB) after QKV / O / gate-up / down: off by default --
-  // measured on the 7B stage: the prefetch traffic slows the latency-bound
-  // attention more than it shortens the next mainloop
-  double pf_mb[4] = {0, 0, 0, 0};
   int att_dbg_ends = 0;
   int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
   cudaStream_t st = nullptr;
@@ -474,37 +470,8 @@ void prof_end(fs_ctx* c, int idx) {
 }
 
 // ---------------------------------------------------------------- launches
-// L2 prefetch plan for the GEMM that follows `g` (DESIGN.md "L2 weight
-// prefetch"): the leading `budget` bytes of nx's weights in nx's own
-// consumption order, skipping the boxes nx's CTAs load into shared memory
-// themselves before their grid dependency resolves
-PfPlan make_pf(const GemmOp* nx, double budget, int stages) {
-  PfPlan p;
-  memset(&p, 0, sizeof(p));
-  if (!nx || budget <= 0) return p;
-  p.kind = nx->split > 0 ? 1 : 2;
-  p.T = nx->sh.n_tiles;
-  p.S = nx->split;
-  p.KB = nx->sh.kb_total;
-  p.U = nx->sh.units;
-  p.G = nx->grid;
-  const int n_cons = p.kind == 1 ? p.T * p.S : p.G;
-  const int per = p.kind == 1 ? p.KB / std::max(1, p.S) : p.U / std::max(1, p.G);
-  p.skip = std::min(stages, per);
-  p.depth = std::min(per - p.skip, (int)(budget / ((double)n_cons * 128 * 64 * 2)));
-  if (p.depth <= 0) p.kind = 0;
-  return p;
-}
-
-double pf_budget(const char* env, double def_mb) {
-  const char* v = getenv(env);
-  return (v ? atof(v) : def_mb) * 1e6;
-}
-
 template <int NT>
-int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* nx, double pf_bytes) {
-  const PfPlan pf = make_pf(nx, pf_bytes, GemmCfg<NT>::STAGES);
-  const CUtensorMap& tmP = (pf.kind && nx) ? nx->ta : g.ta;
+int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -535,7 +502,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* 
     at[1].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 2;
-    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, tmP, sh, ep, pf);
+    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, sh, ep);
     CK_LAUNCH(c);
     return FS_OK;
   }
@@ -557,21 +524,20 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  cudaLaunchKernelEx(&lc, gemm_tc_kernel<NT>, g.ta, g.tb, tmP, sh, ep, pf);
+  cudaLaunchKernelEx(&lc, gemm_tc_kernel<NT>, g.ta, g.tb, sh, ep);
   CK_LAUNCH(c);
   return FS_OK;
 }
 
-int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep, const GemmOp* nx = nullptr,
-                double pf_bytes = 0) {
+int launch_gemm(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   const double bytes = (double)g.sh.n_out * g.sh.K * 2 + 2.0 * c->npad * g.sh.K * 2 +
                        (double)c->h_rows->n_rows * g.sh.n_out * 4;
   const int pi = prof_begin(c, 0, bytes);
   int rc;
   switch (c->npad) {
-    case 16: rc = launch_gemm_nt<16>(c, g, ep, nx, pf_bytes); break;
-    case 32: rc = launch_gemm_nt<32>(c, g, ep, nx, pf_bytes); break;
-    default: rc = launch_gemm_nt<64>(c, g, ep, nx, pf_bytes); break;
+    case 16: rc = launch_gemm_nt<16>(c, g, ep); break;
+    case 32: rc = launch_gemm_nt<32>(c, g, ep); break;
+    default: rc = launch_gemm_nt<64>(c, g, ep); break;
   }
   prof_end(c, pi);
   return rc;
@@ -780,10 +746,7 @@ int layer_forward(fs_ctx* c, int l) {
     e.q_out = (bf16*)c->q;
     e.k_cache = (bf16*)kv_plane(c, l, 0);
     e.v_cache = (bf16*)kv_plane(c, l, 1);
-    e.kv_prefetch = getenv("FS_KV_PF") ? 1 : 0;   // measured: no gain, opt-in
-    // L2 prefetch of the next GEMM's leading weights (keeps HBM busy across
-    // epilogues, transitions and attention); budgets in MB, env-tunable
-    if ((rc = launch_gemm(c, w.qkv, e, &w.o, pf_budget("FS_PF_QKV", c->pf_mb[0])))) return rc;
+    if ((rc = launch_gemm(c, w.qkv, e))) return rc;
     if ((rc = launch_attention(c, l))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
@@ -791,11 +754,11 @@ int layer_forward(fs_ctx* c, int l) {
     e.ssq_out = c->ssq;
     e.z_gain = (const bf16*)w.g2;
     e.z_out = (bf16*)c->y;
-    if ((rc = launch_gemm(c, w.o, e, &w.gu, pf_budget("FS_PF_O", c->pf_mb[1])))) return rc;
+    if ((rc = launch_gemm(c, w.o, e))) return rc;
     e = norm_input(c);
     e.mode = EPI_GLU;
     e.act = (bf16*)c->act;
-    if ((rc = launch_gemm(c, w.gu, e, &w.dn, pf_budget("FS_PF_GU", c->pf_mb[2])))) return rc;
+    if ((rc = launch_gemm(c, w.gu, e))) return rc;
     e = base_epi(c);
     e.mode = EPI_RESID;
     e.x = c->x;
@@ -803,8 +766,7 @@ int layer_forward(fs_ctx* c, int l) {
     e.ssq_out = gn ? c->ssq : nullptr;
     e.z_gain = gn;
     e.z_out = gn ? (bf16*)c->y : nullptr;
-    const GemmOp* nx = (l + 1 < c->nl) ? &c->lw[l + 1].qkv : (c->last ? &c->head : nullptr);
-    if ((rc = launch_gemm(c, w.dn, e, nx, pf_budget("FS_PF_DN", c->pf_mb[3])))) return rc;
+    if ((rc = launch_gemm(c, w.dn, e))) return rc;
   } else {
     float* yf = c->yf;
     rmsnorm_kernel<float, float, false><<<np, 128, 0, c->st>>>(c->x, (const float*)w.g1, (float*)c->y, d,

@@ -90,21 +90,6 @@ FS_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t
       : "memory");
 }
 
-// 2D box global -> L2 only (no shared memory, no completion): a hint that
-// keeps HBM streaming a later kernel's operand while this one drains
-FS_DEV void tma_prefetch_l2_2d(const void* tmap, int32_t x, int32_t y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(tmap)),
-               "r"(x), "r"(y)
-               : "memory");
-}
-
-// contiguous global range -> L2 (bytes: multiple of 16)
-FS_DEV void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
-               : "memory");
-}
-
 // ------------------------------------------------------------ tcgen05 / TMEM
 FS_DEV void tmem_alloc(uint32_t* holder_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

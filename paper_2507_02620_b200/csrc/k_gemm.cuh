@@ -36,33 +36,6 @@ struct GemmShape {
   int late_trigger; // diagnostics: trigger dependents at exit instead of at start
   unsigned long long* dbg;  // optional phase timestamps [cta][8] (diagnostics)
 };
-// L2 prefetch of the NEXT GEMM's leading weight boxes, issued by this GEMM's
-// producer threads once their own last TMA load is out: HBM keeps streaming
-// through this kernel's epilogue, the kernel transition and (after QKV) the
-// attention kernel, and the next GEMM's mainloop starts from L2.  The boxes
-// follow the next GEMM's own consumption order (its work decomposition).
-struct PfPlan {
-  int kind;              // 0 none, 1 cluster split-K consumer, 2 stream-K consumer
-  int T, S, KB, U, G;    // consumer geometry: tiles, split, k-blocks/tile, units, grid
-  int skip, depth;       // per consumer CTA: units [skip, skip + depth) of its range
-};
-FS_DEV void issue_l2_prefetch(const CUtensorMap* tm, const PfPlan& pf, int c, int g_cur) {
-  if (pf.kind == 1) {
-    for (int j = c; j < pf.T * pf.S; j += g_cur) {
-      const int t = j / pf.S, r = j % pf.S;
-      const int kb0 = (int)((long long)r * pf.KB / pf.S), kb1 = (int)((long long)(r + 1) * pf.KB / pf.S);
-      const int e = min(kb1, kb0 + pf.skip + pf.depth);
-      for (int kb = kb0 + pf.skip; kb < e; kb++) tma_prefetch_l2_2d(tm, kb * 64, t * 128);
-    }
-  } else if (pf.kind == 2) {
-    for (int j = c; j < pf.G; j += g_cur) {
-      const int u0 = (int)((long long)j * pf.U / pf.G), u1 = (int)((long long)(j + 1) * pf.U / pf.G);
-      const int e = min(u1, u0 + pf.skip + pf.depth);
-      for (int u = u0 + pf.skip; u < e; u++) tma_prefetch_l2_2d(tm, (u % pf.KB) * 64, (u / pf.KB) * 128);
-    }
-  }
-}
-
 FS_DEV unsigned long long g_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -107,27 +80,7 @@ struct GemmEpi {
   float* ssq_out;           // [n_tiles][npad] or null
   const bf16* z_gain;       // g of the next RMSNorm, or null
   bf16* z_out;
-  // QKV: L2 prefetch of this layer's context K/V rows [0, slot of the first
-  // row) for the attention kernel that follows (HBM is idle during the
-  // epilogue and the kernel transition)
-  int kv_prefetch;
 };
-
-// the producer thread's share of the K/V context prefetch (16 KB pieces)
-FS_DEV void kv_l2_prefetch(const GemmEpi& ep, int c, int g_cur) {
-  const int n_ctx = ep.rows->slot[0];   // keys below the first slot written this tick
-  if (n_ctx <= 0) return;
-  const size_t head_bytes = (size_t)n_ctx * 128 * sizeof(bf16);
-  const int per_head = (int)((head_bytes + 16383) / 16384);
-  const int total = 2 * ep.Hkv * per_head;
-  for (int j = c; j < total; j += g_cur) {
-    const int hp = j / per_head, piece = j % per_head;
-    const bf16* base = (hp < ep.Hkv ? ep.k_cache : ep.v_cache) + (size_t)(hp % ep.Hkv) * ep.max_ctx * 128;
-    const size_t off = (size_t)piece * 16384;
-    const uint32_t len = (uint32_t)min((size_t)16384, head_bytes - off);
-    bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(base) + off, len);
-  }
-}
 
 // The activation operand carries each fp32 value as two bf16 rows (hi, lo:
 // rows [0,NT) and [NT,2NT) of the B tile), so UMMA N = 2*NT and the epilogue
@@ -372,7 +325,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
 template <int NT>
 __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmP, GemmShape sh, GemmEpi ep, PfPlan pfp) {
+                   GemmShape sh, GemmEpi ep) {
   using C = GemmCfg<NT>;
   extern __shared__ uint8_t gsm_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
@@ -397,7 +350,6 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (pfp.kind) tma_prefetch_desc(&tmP);
     for (int s = 0; s < C::STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -452,8 +404,6 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
           phase ^= 1;
         }
       }
-      issue_l2_prefetch(&tmP, pfp, c, G);
-      if (ep.kv_prefetch) kv_l2_prefetch(ep, c, G);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -636,7 +586,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 template <int NT>
 __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const __grid_constant__ CUtensorMap tmP, GemmShape sh, GemmEpi ep, PfPlan pfp) {
+                        GemmShape sh, GemmEpi ep) {
   namespace cg = cooperative_groups;
   using C = GemmCfg<NT>;
   cg::cluster_group cluster = cg::this_cluster();
@@ -664,7 +614,6 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (pfp.kind) tma_prefetch_desc(&tmP);
     for (int s = 0; s < C::STAGES; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -706,8 +655,6 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
           phase ^= 1;
         }
       }
-      issue_l2_prefetch(&tmP, pfp, blockIdx.x, gridDim.x);
-      if (ep.kv_prefetch) kv_l2_prefetch(ep, blockIdx.x, gridDim.x);
     }
     __syncwarp();
   } else if (warp == 1) {
