@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--prefix", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-attn-long", action="store_true")
     return ap.parse_args()
 
 
@@ -352,8 +353,45 @@ def ours(args):
     if P == 1 and not args.no_cpu_baseline:
         rec["cpu_baseline"] = cpu_baseline(shape, trees[0], prefix, ranks, tokens / K, ticks / K,
                                            n_samples=1)
-    emit(rec)
     gp.close()
+    if P == 1 and not args.no_attn_long and "roofline" in rec:
+        try:
+            rec["roofline"]["attention_long_context"] = attention_long_context(hbm)
+        except Exception as ex:   # informative only: never costs the main line
+            rec["roofline"]["attention_long_context"] = {"error": str(ex)[:200]}
+    emit(rec)
+
+
+def attention_long_context(hbm):
+    """Tree attention where its bytes matter ("attention GB/s is
+    meaningful on configs 4-5"): one layer of the configs[3] (13B, 4096-token
+    context, 16-row segment) and configs[4] (72B GQA, 16384-token context,
+    32-row segment) shapes, synthetic-KV prefix, bench_kernel kind 5 = that
+    layer's attention launches back to back (CUDA events).  Achieved = K + V
+    bytes of the context / time."""
+    from paper_2507_02620_b200 import flowspec as F
+    from synth import gen
+    from synth.configs import reduced
+    out = []
+    for name, cfg, ctx, seg in (("13b", "configs[3] 13B MHA", 4096, 16), ("72b", "configs[4] 72B GQA", 16384, 32)):
+        shape = reduced(name, 1)
+        gp = F.Pipeline(shape, max_ctx=ctx + 600, max_seg=seg)
+        try:
+            gp.fs_load_random_weights(SEED)
+            gp.fs_set_prefix(gen.prefix_tokens(SEED, ctx, shape.vocab), F.FS_SYNTH_KV, kv_seed=7)
+            t = gen.random_tree(3, seg, 6, shape.vocab, gp.state()["x_new"])
+            gp.fs_submit_segment(F.FS_NEW_ROUND, t["parent"], t["token"], t["own"], seg)
+            gp.fs_verify_step()
+            us = min(gp.bench_kernel(5, 20)[0] for _ in range(3))
+            n_keys = ctx + seg
+            kv = n_keys * shape.n_kv_heads * shape.head_dim * 2 * 2
+            gbs = kv / (us * 1e-6) / 1e9
+            out.append({"config": f"{cfg}, {n_keys} keys, {seg} query rows", "us_per_layer": round(us, 2),
+                        "kv_bytes": kv, "achieved": round(gbs, 1), "unit": "GB/s",
+                        "frac": round(gbs / hbm, 4)})
+        finally:
+            gp.close()
+    return out
 
 
 # ------------------------------------------------------------------ oracle arm
