@@ -340,7 +340,7 @@ def ours(args):
         rec["roofline"] = {
             "kernel": "gemm_tc_kernel (tcgen05 weight-streaming GEMM, all layers + head)",
             "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
+            "frac": round(ach / hbm, 4), "traffic": ncu_traffic(g_bytes), "peak_source": peak_src,
             "launches_per_step": prof["gemm_launches"],
             "share_of_step": round(prof["gemm_ms"] / prof["step_ms"], 4),
             "attention": {
@@ -360,6 +360,19 @@ def ours(args):
         except Exception as ex:   # informative only: never costs the main line
             rec["roofline"]["attention_long_context"] = {"error": str(ex)[:200]}
     emit(rec)
+
+
+def ncu_traffic(alg_bytes_per_launch):
+    """roofline.traffic: DRAM bytes (read + write) per GEMM launch, from the committed
+    ncu --set full capture of the same build (profiles/r1_ncu_traffic.json: per-class
+    DRAM / algorithmic bytes, weighted over a tick) applied to this run's average
+    algorithmic bytes per launch; null when the capture is absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            ratio = float(json.load(f)["ratio_weighted_per_tick"])
+        return round(alg_bytes_per_launch * ratio)
+    except Exception:
+        return None
 
 
 def attention_long_context(hbm):
