@@ -476,9 +476,12 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          GemmCfg<NT>::SMEM);
-    cudaFuncSetAttribute(gemm_cluster_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          GemmCfg<NT>::SMEM);
-    cudaFuncSetAttribute(gemm_cluster_kernel<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GemmCfg<NT>::SMEM);
+    cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   if (g.split > 0) {
@@ -502,7 +505,11 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
     at[1].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 2;
-    cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT>, g.ta, g.tb, sh, ep);
+    // column window per rank: NT / 2 covers S <= 3, NT / 4 covers S >= 4
+    if (g.split <= 3)
+      cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT, NT / 2>, g.ta, g.tb, sh, ep);
+    else
+      cudaLaunchKernelEx(&lc, gemm_cluster_kernel<NT, NT / 4>, g.ta, g.tb, sh, ep);
     CK_LAUNCH(c);
     return FS_OK;
   }

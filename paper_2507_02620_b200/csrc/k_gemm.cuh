@@ -116,9 +116,9 @@ FS_DEV int cta_of_unit(int u, int units, int G) {
 // epilogue warps while the mainloop streams (they idle until acc_full): the
 // dependent L2 round trips (n_rows -> pos -> rope, bias, slot, residual, gain)
 // then stay off the critical path between the last MMA and the stores.
-template <int NT>
+template <int W>
 struct EpiPre {
-  static constexpr int NP = NT <= 16 ? NT : 1;   // register budget: NT=16 only
+  static constexpr int NP = W <= 16 ? W : 1;   // register budget: windows of <= 16 columns
   int n_rows;
   bool tile;          // bias / gv / x hold tile t's values
   float bias, gv;
@@ -127,95 +127,123 @@ struct EpiPre {
   float x[NP];
 };
 
-template <int NT, bool PFR = true>
+// window j <-> token column mlo + j
+template <int NT, int W, bool PFR = true>
 FS_DEV void epi_prefetch(const GemmShape& sh, const GemmEpi& ep, int t, int row, int mlo, int mhi,
-                         bool tile, EpiPre<NT>& p) {
+                         bool tile, EpiPre<W>& p) {
   const TickRows* rows = ep.rows;
   p.n_rows = rows->n_rows;
   p.tile = tile;
   p.bias = 0.f;
   p.gv = 0.f;
   const int ng = t * 128 + row;
-  const int mend = min(mhi, p.n_rows);
+  const int jend = min(mhi, p.n_rows) - mlo;
   if (ep.mode == EPI_QKV) {
     if (tile && ep.bias) p.bias = to_f32(ep.bias[ng]);
-    if constexpr (PFR && NT <= 16) {
+    if constexpr (PFR && W <= 16) {
       const int i = row & 63;
 #pragma unroll
-      for (int m = 0; m < NT; m++) {
-        const bool live = m >= mlo && m < mend;
-        p.slot[m] = live ? rows->slot[m] : 0;
-        p.cs[m] = live ? ep.rope[(size_t)rows->pos[m] * 64 + i] : make_float2(0.f, 0.f);
+      for (int j = 0; j < W; j++) {
+        const bool live = j < jend;
+        p.slot[j] = live ? rows->slot[mlo + j] : 0;
+        p.cs[j] = live ? ep.rope[(size_t)rows->pos[mlo + j] * 64 + i] : make_float2(0.f, 0.f);
       }
     }
   } else if (ep.mode == EPI_RESID) {
     if (tile && ep.z_gain && ng < sh.n_out) p.gv = __bfloat162float(ep.z_gain[ng]);
-    if constexpr (PFR && NT <= 16) {
+    if constexpr (PFR && W <= 16) {
 #pragma unroll
-      for (int m = 0; m < NT; m++)
-        p.x[m] = (tile && m >= mlo && m < mend && ng < sh.n_out) ? ep.x[(size_t)m * ep.d + ng] : 0.f;
+      for (int j = 0; j < W; j++)
+        p.x[j] = (tile && j < jend && ng < sh.n_out) ? ep.x[(size_t)(mlo + j) * ep.d + ng] : 0.f;
     }
   }
 }
 
-// Fused epilogue for output rows (weights) t*128+row; token columns m in
-// [mlo, mhi) are owned by this call (all NT for stream-K, a share in cluster
-// split-K), v[] holds the fp32 accumulator of every column.
-template <int NT, bool PFR = true>
+// Per-column sums over the 32 lanes (rows) of a warp for W columns: a
+// reduce-scatter butterfly (each step keeps half of the columns and adds the
+// partner lane's copy), then a plain butterfly; the lane's column is returned
+// in col.  W <= 16 shuffles in total, no branches.
+template <int W, int LVL>
+FS_DEV float warp_colsum(const float* v, int lane, int& col) {
+  if constexpr (W == 1) {
+    float z = v[0];
+#pragma unroll
+    for (int o = 16 >> LVL; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    return z;
+  } else {
+    constexpr int O = 16 >> LVL, H = W / 2;
+    const bool up = lane & O;
+    float u[H];
+#pragma unroll
+    for (int k = 0; k < H; k++) {
+      const float send = up ? v[k] : v[k + H];
+      u[k] = (up ? v[k + H] : v[k]) + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    if (up) col += H;
+    return warp_colsum<H, LVL + 1>(u, lane, col);
+  }
+}
+
+// Fused epilogue for output rows (weights) t*128+row and token columns
+// [mlo, mhi): v[j] holds column mlo + j (W = NT, mlo = 0 for stream-K; a
+// W = NT / S window for cluster split-K rank r).
+template <int NT, int W, bool PFR = true>
 FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
-                          float* xch, Top2* stop, int mlo, int mhi, const EpiPre<NT>& p) {
+                          float* xch, Top2* stop, int mlo, int mhi, const EpiPre<W>& p) {
   const TickRows* rows = ep.rows;
   const int n_rows = p.n_rows;
-  constexpr bool PF = PFR && NT <= 16;   // per-row operands prefetched (cluster kernel)
+  constexpr bool PF = PFR && W <= 16;   // per-row operands prefetched
   const int ng = t * 128 + row;
   const int lane = lane_id(), q = warp_id() & 3;
-  const int mend = min(mhi, n_rows);
+  const int jend = min(mhi, n_rows) - mlo, jhi = mhi - mlo;
   if (ep.mode == EPI_QKV) {
     const int H = ep.H, Hkv = ep.Hkv;
     if (ep.bias) {
       const float b = p.tile ? p.bias : to_f32(ep.bias[ng]);
 #pragma unroll
-      for (int m = 0; m < NT; m++) v[m] += b;
+      for (int j = 0; j < W; j++) v[j] += b;
     }
     const int hh = t;  // one head (128 rows) per tile
     if (hh < H + Hkv) {  // rotate-half RoPE on q and k heads (partner row ^ 64)
 #pragma unroll
-      for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
+      for (int j = 0; j < W; j++) xch[row * (W + 1) + j] = v[j];
       named_bar_sync(1, 128);
       const int i = row & 63;
 #pragma unroll
-      for (int m = 0; m < NT; m++) {
-        const float pv = xch[(row ^ 64) * (NT + 1) + m];
-        if (m >= mlo && m < mend) {
-          const float2 cs = PF ? p.cs[PF ? m : 0] : ep.rope[(size_t)rows->pos[m] * 64 + i];
-          v[m] = (row < 64) ? (v[m] * cs.x - pv * cs.y) : (v[m] * cs.x + pv * cs.y);
+      for (int j = 0; j < W; j++) {
+        const float pv = xch[(row ^ 64) * (W + 1) + j];
+        if (j < jend) {
+          const float2 cs = PF ? p.cs[PF ? j : 0] : ep.rope[(size_t)rows->pos[mlo + j] * 64 + i];
+          v[j] = (row < 64) ? (v[j] * cs.x - pv * cs.y) : (v[j] * cs.x + pv * cs.y);
         }
       }
       named_bar_sync(1, 128);
     }
 #pragma unroll
-    for (int m = 0; m < NT; m++) {
-      if (m < mlo || m >= mend) continue;
-      const bf16 o = __float2bfloat16_rn(v[m]);
+    for (int j = 0; j < W; j++) {
+      if (j >= jend) continue;
+      const int m = mlo + j;
+      const bf16 o = __float2bfloat16_rn(v[j]);
       if (hh < H) {
         ep.q_out[((size_t)m * H + hh) * 128 + row] = o;
       } else if (hh < H + Hkv) {
-        const int sl = PF ? p.slot[PF ? m : 0] : rows->slot[m];
+        const int sl = PF ? p.slot[PF ? j : 0] : rows->slot[m];
         ep.k_cache[((size_t)(hh - H) * ep.max_ctx + sl) * 128 + row] = o;
       } else {
-        const int sl = PF ? p.slot[PF ? m : 0] : rows->slot[m];
+        const int sl = PF ? p.slot[PF ? j : 0] : rows->slot[m];
         ep.v_cache[((size_t)(hh - H - Hkv) * ep.max_ctx + sl) * 128 + row] = o;
       }
     }
   } else if (ep.mode == EPI_GLU) {
 #pragma unroll
-    for (int m = 0; m < NT; m++) xch[row * (NT + 1) + m] = v[m];
+    for (int j = 0; j < W; j++) xch[row * (W + 1) + j] = v[j];
     named_bar_sync(1, 128);
     if (row < 64) {
 #pragma unroll
-      for (int m = 0; m < NT; m++) {
-        if (m < mlo || m >= mend) continue;
-        const float g = v[m], u = xch[(row + 64) * (NT + 1) + m];
+      for (int j = 0; j < W; j++) {
+        if (j >= jend) continue;
+        const int m = mlo + j;
+        const float g = v[j], u = xch[(row + 64) * (W + 1) + j];
         const float a = g / (1.0f + expf(-g)) * u;
         const bf16 hi = __float2bfloat16_rn(a);
         ep.act[(size_t)m * ep.ffn + t * 64 + row] = hi;
@@ -224,29 +252,30 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     }
     named_bar_sync(1, 128);
   } else if (ep.mode == EPI_RESID) {
-    float sq[NT], xn[NT];
+    float sq[W], xn[W];
     // old residual values first (all loads in flight), then the update
 #pragma unroll
-    for (int m = 0; m < NT; m++) {
-      xn[m] = 0.f;
-      if (m >= mlo && m < mend && ng < sh.n_out) xn[m] = (PF && p.tile) ? p.x[PF ? m : 0] : ep.x[(size_t)m * ep.d + ng];
+    for (int j = 0; j < W; j++) {
+      xn[j] = 0.f;
+      if (j < jend && ng < sh.n_out) xn[j] = (PF && p.tile) ? p.x[PF ? j : 0] : ep.x[(size_t)(mlo + j) * ep.d + ng];
     }
 #pragma unroll
-    for (int m = 0; m < NT; m++) {
-      sq[m] = 0.f;
-      if (m >= mlo && m < mend && ng < sh.n_out) {
-        xn[m] += v[m];
-        ep.x[(size_t)m * ep.d + ng] = xn[m];
-        sq[m] = xn[m] * xn[m];
+    for (int j = 0; j < W; j++) {
+      sq[j] = 0.f;
+      if (j < jend && ng < sh.n_out) {
+        xn[j] += v[j];
+        ep.x[(size_t)(mlo + j) * ep.d + ng] = xn[j];
+        sq[j] = xn[j] * xn[j];
       }
     }
     if (threadIdx.x == 64 && sh.dbg) GEMM_PROBE(10);
     if (ep.z_out && ng < sh.n_out) {  // next norm's B operand: x_new * g as a bf16 hi/lo pair
       const float gv = p.tile ? p.gv : __bfloat162float(ep.z_gain[ng]);
 #pragma unroll
-      for (int m = 0; m < NT; m++) {
-        if (m < mlo || m >= mhi) continue;
-        const float zv = (m < n_rows) ? xn[m] * gv : 0.f;
+      for (int j = 0; j < W; j++) {
+        if (j >= jhi) continue;
+        const int m = mlo + j;
+        const float zv = (m < n_rows) ? xn[j] * gv : 0.f;
         const bf16 hi = __float2bfloat16_rn(zv);
         ep.z_out[(size_t)m * ep.d + ng] = hi;
         ep.z_out[(size_t)(NT + m) * ep.d + ng] = __float2bfloat16_rn(zv - __bfloat162float(hi));
@@ -255,40 +284,18 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     if (threadIdx.x == 64 && sh.dbg) GEMM_PROBE(11);
     if (ep.ssq_out) {  // deterministic sums of squares of the new residual rows: one
       // partial per warp (32 output columns); the consumer sums d / 32 of them
-      if constexpr (NT == 16) {
-        // reduce-scatter butterfly: every step keeps half of the columns and adds
-        // the partner lane's copy of them (16 shuffles for all 16 columns, no
-        // branches); lane ends with column ((l>>4)&1)*8 + ((l>>3)&1)*4 + ((l>>2)&1)*2 + ((l>>1)&1)
-        float w8[8], w4[4], w2[2];
-        const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4, u2 = lane & 2;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const float send = u16 ? sq[k] : sq[k + 8];
-          w8[k] = (u16 ? sq[k + 8] : sq[k]) + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          const float send = u8 ? w8[k] : w8[k + 4];
-          w4[k] = (u8 ? w8[k + 4] : w8[k]) + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-          const float send = u4 ? w4[k] : w4[k + 2];
-          w2[k] = (u4 ? w4[k + 2] : w4[k]) + __shfl_xor_sync(0xffffffffu, send, 4);
-        }
-        const float send = u2 ? w2[0] : w2[1];
-        float z = (u2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
-        z += __shfl_xor_sync(0xffffffffu, z, 1);
-        const int col = (u16 ? 8 : 0) + (u8 ? 4 : 0) + (u4 ? 2 : 0) + (u2 ? 1 : 0);
-        if (!(lane & 1) && col >= mlo && col < mhi) ep.ssq_out[((size_t)t * 4 + q) * NT + col] = z;
+      if constexpr (W <= 16) {
+        int col = 0;
+        const float z = warp_colsum<W, 0>(sq, lane, col);
+        if ((lane % (32 / W)) == 0 && col < jhi) ep.ssq_out[((size_t)t * 4 + q) * NT + mlo + col] = z;
       } else {
 #pragma unroll
-        for (int m = 0; m < NT; m++) {
-          if (m < mlo || m >= mhi) continue;
-          float z = sq[m];
+        for (int j = 0; j < W; j++) {
+          if (j >= jhi) continue;
+          float z = sq[j];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-          if (lane == 0) ep.ssq_out[((size_t)t * 4 + q) * NT + m] = z;
+          if (lane == 0) ep.ssq_out[((size_t)t * 4 + q) * NT + mlo + j] = z;
         }
       }
     }
@@ -296,29 +303,29 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     const bool valid = ng < ep.vocab;
     if (ep.logits && valid)
 #pragma unroll
-      for (int m = 0; m < NT; m++)
-        if (m >= mlo && m < mend) ep.logits[(size_t)m * ep.vocab + ng] = v[m];
+      for (int j = 0; j < W; j++)
+        if (j < jend) ep.logits[(size_t)(mlo + j) * ep.vocab + ng] = v[j];
 #pragma unroll
-    for (int m = 0; m < NT; m++) {
+    for (int j = 0; j < W; j++) {
       Top2 tt;
-      tt.v1 = valid ? v[m] : -INFINITY;
+      tt.v1 = valid ? v[j] : -INFINITY;
       tt.i1 = valid ? ng : 0x7fffffff;
       tt.v2 = -INFINITY;
       tt = top2_warp(tt);
-      if (lane == 0) stop[q * NT + m] = tt;
+      if (lane == 0) stop[q * W + j] = tt;
     }
     named_bar_sync(1, 128);
-    if (row >= mlo && row < mhi) {
+    if (row < jhi) {
       Top2 r = stop[row];
-      for (int w = 1; w < 4; w++) r = top2_merge(r, stop[w * NT + row]);
-      ep.head_part[(size_t)t * NT + row] = r;
+      for (int w = 1; w < 4; w++) r = top2_merge(r, stop[w * W + row]);
+      ep.head_part[(size_t)t * NT + mlo + row] = r;
     }
     named_bar_sync(1, 128);
   } else {  // EPI_STORE
     if (ng < sh.n_out)
 #pragma unroll
-      for (int m = 0; m < NT; m++)
-        if (m >= mlo && m < mend) ep.out[(size_t)m * ep.ldo + ng] = v[m];
+      for (int j = 0; j < W; j++)
+        if (j < jend) ep.out[(size_t)(mlo + j) * ep.ldo + ng] = v[j];
   }
 }
 
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     // their reads of this epilogue's outputs are done); then prefetch
     pdl_wait();
     EpiPre<NT> pf;
-    epi_prefetch<NT, false>(sh, ep, 0, row, 0, NT, false, pf);
+    epi_prefetch<NT, NT, false>(sh, ep, 0, row, 0, NT, false, pf);
     if (ep.scale_ssq) {
       // inv[m] of the RMSNorm applied by linearity (rows >= n_rows: padding)
       if (row < NT) {
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 #pragma unroll
           for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
         }
-        gemm_epilogue<NT, false>(sh, ep, t, row, v, xch, stop, 0, NT, pf);
+        gemm_epilogue<NT, NT, false>(sh, ep, t, row, v, xch, stop, 0, NT, pf);
       }
       if (threadIdx.x == 64) GEMM_PROBE(9 + 2 * (seg & 1));
       u = seg_end;
@@ -583,7 +590,8 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 // sums the S partials of its share of token columns through distributed
 // shared memory (rank order: deterministic) and runs the fused epilogue for
 // them.  No global partials, atomics or fences on the epilogue path.
-template <int NT>
+// W: the per-rank column window (>= ceil(NT / S)): NT / 2 for S <= 3, NT / 4 for S >= 4
+template <int NT, int W>
 __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         GemmShape sh, GemmEpi ep) {
@@ -628,7 +636,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   if (!sh.late_trigger) pdl_trigger();
-  EpiPre<NT> pf;
+  EpiPre<W> pf;
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer: weights before the grid dependency, activations after
@@ -686,11 +694,11 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     pdl_wait();
-    epi_prefetch<NT>(sh, ep, t, row, r * NT / S, (r + 1) * NT / S, true, pf);
+    epi_prefetch<NT, W>(sh, ep, t, row, r * NT / S, (r + 1) * NT / S, true, pf);
     if (threadIdx.x == 64 && sh.dbg) {  // diagnostics: prefetched operands have landed
       float z = pf.gv + pf.bias;
 #pragma unroll
-      for (int m = 0; m < EpiPre<NT>::NP; m++) z += pf.x[m] + pf.cs[m].x + (float)pf.slot[m];
+      for (int m = 0; m < EpiPre<W>::NP; m++) z += pf.x[m] + pf.cs[m].x + (float)pf.slot[m];
       if (z == 12345.f) sh.dbg[0] = 0;
       GEMM_PROBE(7);
     }
@@ -728,23 +736,19 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
         if (threadIdx.x == 64) GEMM_PROBE(8);
       }
       const int mlo = r * NT / S, mhi = pass ? (r + 1) * NT / S : mlo;
-      float v[NT];
+      // DSMEM partials of every rank for my column window: issue up to 4
+      // ranks' loads together, accumulate in rank order (deterministic)
+      float acc[W];
 #pragma unroll
-      for (int m = 0; m < NT; m++) v[m] = 0.f;
-      // DSMEM partials of every rank for my columns: issue up to 4 ranks' loads
-      // together, accumulate in rank order (deterministic)
-      constexpr int MW = (NT + 1) / 2;   // max columns per rank (S >= 2)
-      float acc[MW];
-#pragma unroll
-      for (int j = 0; j < MW; j++) acc[j] = 0.f;
+      for (int j = 0; j < W; j++) acc[j] = 0.f;
       for (int c0 = 0; c0 < S; c0 += 4) {
-        float pv[4][MW];
+        float pv[4][W];
 #pragma unroll
         for (int cc = 0; cc < 4; cc++) {
           if (c0 + cc < S) {
             const uint32_t pc = dsmem_addr(part + mlo * 128 + row, (uint32_t)(c0 + cc));
 #pragma unroll
-            for (int j = 0; j < MW; j++)
+            for (int j = 0; j < W; j++)
               if (mlo + j < mhi) pv[cc][j] = ld_dsmem_f32(pc + j * 128 * 4);
           }
         }
@@ -752,30 +756,20 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
         for (int cc = 0; cc < 4; cc++) {
           if (c0 + cc < S) {
 #pragma unroll
-            for (int j = 0; j < MW; j++) acc[j] += (mlo + j < mhi) ? pv[cc][j] : 0.f;
+            for (int j = 0; j < W; j++) acc[j] += (mlo + j < mhi) ? pv[cc][j] : 0.f;
           }
         }
       }
       if (threadIdx.x == 64 && sh.dbg) {  // diagnostics: DSMEM loads complete
-        if (acc[0] + acc[MW - 1] == 12345.f) sh.dbg[1] = 0;
+        if (acc[0] + acc[W - 1] == 12345.f) sh.dbg[1] = 0;
         GEMM_PROBE(9);
-      }
-      // scatter acc[j] -> v[mlo + j] with static register indices
-#pragma unroll
-      for (int m = 0; m < NT; m++)
-#pragma unroll
-        for (int j = 0; j < MW; j++)
-          if (m == mlo + j && m < mhi) v[m] = acc[j];
-      if (threadIdx.x == 64 && sh.dbg) {
-        if (v[0] + v[NT - 1] == 12345.f) sh.dbg[1] = 0;
-        GEMM_PROBE(12);
       }
       if (ep.scale_ssq) {
         named_bar_sync(1, 128);  // s_inv visible to all epilogue warps
 #pragma unroll
-        for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+        for (int j = 0; j < W; j++) acc[j] *= s_inv[min(mlo + j, NT - 1)];
       }
-      gemm_epilogue<NT>(sh, ep, t, row, v, xch, stop, mlo, mhi, pf);
+      gemm_epilogue<NT, W>(sh, ep, t, row, acc, xch, stop, mlo, mhi, pf);
     }
   }
   // matches the epilogue warps' pass-1 barrier (these warps published nothing)
