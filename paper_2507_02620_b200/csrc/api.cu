@@ -264,13 +264,20 @@ void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const ch
   g.sh.units = g.sh.n_tiles * g.sh.kb_total;
   g.sh.late_trigger = getenv("FS_LATE_TRIGGER") ? 1 : 0;
   g.grid = std::min(n_sms, g.sh.units);
-  // Few output tiles: tile-aligned cluster split-K with S = floor(SMs / tiles)
-  // CTAs per tile (one wave using one CTA slot per SM, so the next kernel's CTA
-  // can be resident and prefetch its weights); S = 2 when tiles fit one wave
-  // and two CTAs fit per SM.  Many tiles: stream-K.  (Measured on the 7B stage
-  // forward: QKV 2, O 4, down 4, gate/up and head stream-K; 3.96 ms vs 4.47 ms
-  // all stream-K.)
-  int S = n_sms / std::max(1, g.sh.n_tiles);
+  // Few output tiles: tile-aligned cluster split-K with S CTAs per tile.  Two
+  // CTAs fit per SM (NT 16): S = the largest power of two keeping the grid in
+  // one wave of 2 x SMs slots; otherwise S = floor(SMs / tiles).  Many tiles:
+  // stream-K.  (Measured on the 7B stage forward with windowed epilogues:
+  // QKV 2, O 8, down 8, gate/up and head stream-K -- 3.02 ms vs 3.11 ms with
+  // O / down at 4, 3.44 ms at 16.)
+  int S;
+  if (ctas_per_sm >= 2) {
+    const int cap = ctas_per_sm * n_sms / std::max(1, g.sh.n_tiles);
+    S = 1;
+    while (S * 2 <= cap) S *= 2;
+  } else {
+    S = n_sms / std::max(1, g.sh.n_tiles);
+  }
   if (S < 2 && ctas_per_sm >= 2 && g.sh.n_tiles <= n_sms) S = 2;
   S = std::min({S, 16, g.sh.kb_total});
   g.split = (S >= 2 && !getenv("FS_NO_CLUSTER_GEMM")) ? S : 0;
