@@ -263,6 +263,8 @@ void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const ch
   g.sh.n_tiles = (n_out + 127) / 128;
   g.sh.units = g.sh.n_tiles * g.sh.kb_total;
   g.sh.late_trigger = getenv("FS_LATE_TRIGGER") ? 1 : 0;
+  // stream-K: one CTA per SM (two per SM measured 3.15 vs 2.92 ms per 7B tick:
+  // the next GEMM's CTAs then find no free slot to prefetch into)
   g.grid = std::min(n_sms, g.sh.units);
   // Few output tiles: tile-aligned cluster split-K with S CTAs per tile.  Two
   // CTAs fit per SM (NT 16): S = the largest power of two keeping the grid in
@@ -299,14 +301,16 @@ size_t carve(fs_ctx* c, char* base) {
             V = f.vocab;
   const int nq = (H + 2 * Hkv) * hd;
   const int es = c->esz;
+  // bf16 GEMM weights are box-tiled (gen_weight_kernel): rows padded to 128
+  auto wr = [&](int64_t r) -> size_t { return (size_t)(c->bf ? (r + 127) / 128 * 128 : r); };
   c->lw.assign(c->nl, LayerW());
   for (int l = 0; l < c->nl; l++) {
     LayerW& w = c->lw[l];
-    w.wqkv = cv.take<char>((size_t)nq * d * es);
+    w.wqkv = cv.take<char>(wr(nq) * d * es);
     if (f.qkv_bias) w.bqkv = cv.take<char>((size_t)nq * es);
-    w.wo = cv.take<char>((size_t)d * H * hd * es);
-    w.wgu = cv.take<char>((size_t)2 * ffn * d * es);
-    w.wd = cv.take<char>((size_t)d * ffn * es);
+    w.wo = cv.take<char>(wr(d) * H * hd * es);
+    w.wgu = cv.take<char>(wr(2 * ffn) * d * es);
+    w.wd = cv.take<char>(wr(d) * ffn * es);
     w.g1 = cv.take<char>((size_t)d * es);
     w.g2 = cv.take<char>((size_t)d * es);
     plan_gemm(w.qkv, nq, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_QKV");
@@ -316,7 +320,7 @@ size_t carve(fs_ctx* c, char* base) {
   }
   c->emb = c->first ? cv.take<char>((size_t)V * d * es) : nullptr;
   if (c->last) {
-    c->wh = cv.take<char>((size_t)V * d * es);
+    c->wh = cv.take<char>(wr(V) * d * es);
     c->gf = cv.take<char>((size_t)d * es);
     plan_gemm(c->head, V, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_HEAD");
   }
@@ -407,7 +411,15 @@ bool setup_ctx(fs_ctx* c, const fs_config* f) {
 }
 
 bool encode_map(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                uint32_t box_outer, bool f32 = false) {
+                uint32_t box_outer, bool f32 = false);
+
+// box-tiled weight [ceil(R/128)][K/64][128][64]: a 64-wide map whose row u*128 is box u
+bool encode_wmap(CUtensorMap* m, void* ptr, uint64_t K, uint64_t R) {
+  return encode_map(m, ptr, 64, (R + 127) / 128 * 128 * (K / 64), 64, 128);
+}
+
+bool encode_map(CUtensorMap* m, void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                uint32_t box_outer, bool f32) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -428,13 +440,13 @@ bool build_maps(fs_ctx* c) {
   const int nq = (H + 2 * Hkv) * hd, np = c->npad;
   bool ok = true;
   for (auto& w : c->lw) {
-    ok &= encode_map(&w.qkv.ta, w.wqkv, d, nq, 64, 128);
+    ok &= encode_wmap(&w.qkv.ta, w.wqkv, d, nq);
     ok &= encode_map(&w.qkv.tb, c->y, d, 2 * np, 64, 2 * np);
-    ok &= encode_map(&w.o.ta, w.wo, H * hd, d, 64, 128);
+    ok &= encode_wmap(&w.o.ta, w.wo, H * hd, d);
     ok &= encode_map(&w.o.tb, c->att, H * hd, 2 * np, 64, 2 * np);
-    ok &= encode_map(&w.gu.ta, w.wgu, d, 2 * ffn, 64, 128);
+    ok &= encode_wmap(&w.gu.ta, w.wgu, d, 2 * ffn);
     ok &= encode_map(&w.gu.tb, c->y, d, 2 * np, 64, 2 * np);
-    ok &= encode_map(&w.dn.ta, w.wd, ffn, d, 64, 128);
+    ok &= encode_wmap(&w.dn.ta, w.wd, ffn, d);
     ok &= encode_map(&w.dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
 
     w.qkv.ok = w.o.ok = w.gu.ok = w.dn.ok = ok;
@@ -446,7 +458,7 @@ bool build_maps(fs_ctx* c) {
     ok &= encode_map(&w.tv, kv_plane(c, l, 1), hd, kv_rows, 64, 128);
   }
   if (c->last) {
-    ok &= encode_map(&c->head.ta, c->wh, d, f.vocab, 64, 128);
+    ok &= encode_wmap(&c->head.ta, c->wh, d, f.vocab);
     ok &= encode_map(&c->head.tb, c->y, d, 2 * np, 64, 2 * np);
 
     c->head.ok = ok;
@@ -1034,25 +1046,33 @@ int fs_load_random_weights(fs_ctx* c, uint64_t seed) {
     return gain ? (float)(0.1 / 16777216.0) : (float)(sigma * std::sqrt(3.0) / 16777216.0);
   };
   auto gen = [&](void* dst, uint64_t tid, double sigma, int gain, int64_t rows, int64_t cols,
-                 int mode, int64_t off) -> int {
+                 int mode, int64_t off, int tiled = 0) -> int {
+    tiled &= c->bf ? 1 : 0;
     const int64_t n = rows * cols;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
     if (c->bf)
       gen_weight_kernel<bf16><<<blocks, 256, 0, c->st>>>((bf16*)dst, key(tid), scale(sigma, gain), gain,
-                                                         rows, cols, mode, off);
+                                                         rows, cols, mode, off, tiled);
     else
       gen_weight_kernel<float><<<blocks, 256, 0, c->st>>>((float*)dst, key(tid), scale(sigma, gain),
-                                                          gain, rows, cols, mode, off);
+                                                          gain, rows, cols, mode, off, 0);
     CK_LAUNCH(c);
     return FS_OK;
   };
   const double s = 0.02, so = 0.02 / std::sqrt(2.0 * L);
+  // a ragged last 128-row box of a tiled weight: zero its padding rows
+  auto pad0 = [&](void* p, int64_t R, int64_t K) {
+    if (c->bf && R % 128) cudaMemsetAsync((char*)p + (size_t)(R / 128) * 128 * K * 2, 0, (size_t)128 * K * 2, c->st);
+  };
   for (int l = 0; l < c->nl; l++) {
     const uint64_t gl = (uint64_t)(c->L0 + l) * 16;
     LayerW& w = c->lw[l];
-    if ((rc = gen(w.wqkv, gl + 0, s, 0, (int64_t)H * hd, d, 0, 0))) return rc;
-    if ((rc = gen(w.wqkv, gl + 1, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)H * hd))) return rc;
-    if ((rc = gen(w.wqkv, gl + 2, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)(H + Hkv) * hd))) return rc;
+    pad0(w.wqkv, (int64_t)(H + 2 * Hkv) * hd, d);
+    pad0(w.wo, d, (int64_t)H * hd);
+    pad0(w.wd, d, ffn);
+    if ((rc = gen(w.wqkv, gl + 0, s, 0, (int64_t)H * hd, d, 0, 0, 1))) return rc;
+    if ((rc = gen(w.wqkv, gl + 1, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)H * hd, 1))) return rc;
+    if ((rc = gen(w.wqkv, gl + 2, s, 0, (int64_t)Hkv * hd, d, 0, (int64_t)(H + Hkv) * hd, 1))) return rc;
     if (f.qkv_bias) {
       if ((rc = gen(w.bqkv, gl + 9, s, 0, 1, (int64_t)H * hd, 0, 0))) return rc;
       char* bk = (char*)w.bqkv + (size_t)H * hd * c->esz;
@@ -1060,16 +1080,17 @@ int fs_load_random_weights(fs_ctx* c, uint64_t seed) {
       char* bv = bk + (size_t)Hkv * hd * c->esz;
       if ((rc = gen(bv, gl + 11, s, 0, 1, (int64_t)Hkv * hd, 0, 0))) return rc;
     }
-    if ((rc = gen(w.wo, gl + 3, so, 0, d, (int64_t)H * hd, 0, 0))) return rc;
-    if ((rc = gen(w.wgu, gl + 4, s, 0, ffn, d, 1, 0))) return rc;
-    if ((rc = gen(w.wgu, gl + 5, s, 0, ffn, d, 2, 0))) return rc;
-    if ((rc = gen(w.wd, gl + 6, so, 0, d, ffn, 0, 0))) return rc;
+    if ((rc = gen(w.wo, gl + 3, so, 0, d, (int64_t)H * hd, 0, 0, 1))) return rc;
+    if ((rc = gen(w.wgu, gl + 4, s, 0, ffn, d, 1, 0, 1))) return rc;
+    if ((rc = gen(w.wgu, gl + 5, s, 0, ffn, d, 2, 0, 1))) return rc;
+    if ((rc = gen(w.wd, gl + 6, so, 0, d, ffn, 0, 0, 1))) return rc;
     if ((rc = gen(w.g1, gl + 7, 0, 1, 1, d, 0, 0))) return rc;
     if ((rc = gen(w.g2, gl + 8, 0, 1, 1, d, 0, 0))) return rc;
   }
   if (c->first && (rc = gen(c->emb, 0xFFFF0, s, 0, V, d, 0, 0))) return rc;
   if (c->last) {
-    if ((rc = gen(c->wh, 0xFFFF1, 2.0 / std::sqrt((double)d), 0, V, d, 0, 0))) return rc;
+    pad0(c->wh, V, d);
+    if ((rc = gen(c->wh, 0xFFFF1, 2.0 / std::sqrt((double)d), 0, V, d, 0, 0, 1))) return rc;
     if ((rc = gen(c->gf, 0xFFFF2, 0, 1, 1, d, 0, 0))) return rc;
   }
   rope_table_kernel<<<148 * 4, 256, 0, c->st>>>(c->rope, f.max_ctx, hd / 2, f.rope_theta, hd);

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       for (int i = 0; i < pre; i++) {
         const int u = u0 + i;
         mbar_arrive_expect_tx(&full[i], tx);
-        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (u % KB) * 64, (u / KB) * 128, polA);
+        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], 0, u * 128, polA);  // box-tiled weights: box u
       }
       GEMM_PROBE(1);
       pdl_wait();  // activations / residual are produced by the previous kernel
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       for (int u = u0 + pre; u < u1; u++) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], tx);
-        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], (u % KB) * 64, (u / KB) * 128, polA);
+        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], 0, u * 128, polA);
         tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], (u % KB) * 64, 0, polB);
         if (++stage == C::STAGES) {
           stage = 0;
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
       const int pre = min(nu, C::STAGES);
       for (int i = 0; i < pre; i++) {
         mbar_arrive_expect_tx(&full[i], C::STAGE_BYTES);
-        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], (kb0 + i) * 64, t * 128, polA);
+        tma_load_2d(sA + i * C::A_BYTES, &tmA, &full[i], 0, (t * KB + kb0 + i) * 128, polA);
       }
       GEMM_PROBE(1);
       pdl_wait();
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(192, GemmCfg<NT>::MIN_CTAS)
       for (int i = pre; i < nu; i++) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], (kb0 + i) * 64, t * 128, polA);
+        tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], 0, (t * KB + kb0 + i) * 128, polA);
         tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], (kb0 + i) * 64, 0, polB);
         if (++stage == C::STAGES) {
           stage = 0;

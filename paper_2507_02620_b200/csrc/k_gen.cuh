@@ -20,10 +20,12 @@ FS_DEV float gen_value(uint64_t key, uint64_t e, float c, int gain) {
 }
 
 // row_mode: 0 identity (dst row = row_off + r); 1 / 2: gate / up rows of the
-// 64-row interleaved gate|up matrix (dst row = (r/64)*128 + r%64 (+64 for up))
+// 64-row interleaved gate|up matrix (dst row = (r/64)*128 + r%64 (+64 for up)).
+// tiled: GEMM weight in the TMA-box-major layout [rows/128][cols/64][128][64]
+// (one 16 KB contiguous block per 128 x 64 box; cols % 64 == 0)
 template <typename T>
 __global__ void gen_weight_kernel(T* dst, uint64_t key, float c, int gain, int64_t rows,
-                                  int64_t cols, int row_mode, int64_t row_off) {
+                                  int64_t cols, int row_mode, int64_t row_off, int tiled) {
   const int64_t n = rows * cols;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -31,7 +33,9 @@ __global__ void gen_weight_kernel(T* dst, uint64_t key, float c, int gain, int64
     int64_t dr = row_off + r;
     if (row_mode == 1) dr = (r / 64) * 128 + (r % 64);
     if (row_mode == 2) dr = (r / 64) * 128 + 64 + (r % 64);
-    dst[dr * cols + k] = from_f32<T>(gen_value(key, (uint64_t)idx, c, gain));
+    const int64_t o = tiled ? (((dr >> 7) * (cols >> 6) + (k >> 6)) << 13) + ((dr & 127) << 6) + (k & 63)
+                            : dr * cols + k;
+    dst[o] = from_f32<T>(gen_value(key, (uint64_t)idx, c, gain));
   }
 }
 
