@@ -472,6 +472,32 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       const int t = u / KB;
       const int seg_start = u, seg_end = min(u1, (t + 1) * KB);
       const int buf = seg & 1;
+      const bool whole = (seg_start == t * KB) && (seg_end == (t + 1) * KB);
+      const int cf = whole ? c : cta_of_unit(t * KB, U, G);
+      const int cl = whole ? c : cta_of_unit((t + 1) * KB - 1, U, G);
+      const int j = c - cf, nc = cl - cf + 1;
+      // Two contributors (the common case: a CTA's run is longer than a tile):
+      // the head contributor j = 0 always finishes the tile.  Its head segment
+      // is the last of its run while the tail contributor's is the first of
+      // its, so the partial is published long before; the head's epilogue
+      // warps wait for it and pull it into registers while the MMA still
+      // streams, keeping both L2 round trips off the tail.
+      float pre[NT];
+      if (nc == 2 && j == 0) {
+        if (warp == 2 && lane == 0)
+          while (ld_acquire_gpu(&sh.counters[t]) < 1) __nanosleep(64);
+        named_bar_sync(1, 128);
+        const float* rp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
+#pragma unroll
+        for (int m = 0; m < NT / 4; m++) {
+          const float4 q4 = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+          pre[4 * m] = q4.x;
+          pre[4 * m + 1] = q4.y;
+          pre[4 * m + 2] = q4.z;
+          pre[4 * m + 3] = q4.w;
+        }
+        if (warp == 2 && lane == 0) sh.counters[t] = 0;
+      }
       mbar_wait(&acc_full[buf], (seg >> 1) & 1);
       tc_fence_after();
       float v[NT];
@@ -488,12 +514,24 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
       if (threadIdx.x == 64) GEMM_PROBE(8 + 2 * (seg & 1));
-      const bool whole = (seg_start == t * KB) && (seg_end == (t + 1) * KB);
       bool run_epi = whole;
-      if (!whole) {
-        const int cf = cta_of_unit(t * KB, U, G);
-        const int cl = cta_of_unit((t + 1) * KB - 1, U, G);
-        const int j = c - cf, nc = cl - cf + 1;
+      if (nc == 2) {
+        if (j == 0) {
+#pragma unroll
+          for (int m = 0; m < NT; m++) v[m] += pre[m];   // own + partial 1: contributor order
+          run_epi = true;
+        } else {  // tail contributor: publish (one gpu-scope release) and leave
+          float* wp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
+#pragma unroll
+          for (int m = 0; m < NT; m += 4)
+            __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+          named_bar_sync(1, 128);
+          if (warp == 2 && lane == 0) {
+            __threadfence();
+            atomicAdd(&sh.counters[t], 1);
+          }
+        }
+      } else if (!whole) {
         // every other contributor already published (the common case for the CTA
         // finishing a tile last): reduce from registers, no partial round trip
         if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
