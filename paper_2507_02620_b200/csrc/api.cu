@@ -136,6 +136,7 @@ struct fs_ctx {
   Seg slot[FS_MAX_STAGES];
   int n_cached[FS_MAX_STAGES] = {0};
   bool weights = false, poisoned = false, prefixed = false;
+  bool plan_ready = false;   // h_rec->spec_* match the tree (set by the verify step's accept)
   std::string err;
   uint64_t launches = 0;
   float* logits_buf = nullptr;
@@ -1111,6 +1112,7 @@ int fs_set_logits_buffer(fs_ctx* c, float* dev_logits, int32_t rows_cap) {
 
 static void reset_round(fs_ctx* c) {
   c->acc_ready = false;
+  c->plan_ready = false;
   c->live = 0;
   c->n_live = 0;
   c->next_id = 0;
@@ -1219,6 +1221,7 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
     return fail(c, FS_EINVAL, "bad submit arguments");
   const bool nr = kind == FS_NEW_ROUND;
   c->acc_ready = false;
+  c->plan_ready = false;
   if (nr && c->live) return fail(c, FS_ESTATE, "round live");
   if (!nr && !c->live) return fail(c, FS_ESTATE, "no live round");
   const int base = nr ? 0 : c->next_id;
@@ -1320,11 +1323,15 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     CK_CUDA(c, cudaMemcpyAsync(c->h_node, c->out_node, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
     // the accept walk (fs_accept) over the updated tree, under the same sync
     c->acc_ready = false;
+    c->plan_ready = false;
     if (c->live && c->n_live > 0) {
       accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
       CK_LAUNCH(c);
+      prune_plan_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live);
+      CK_LAUNCH(c);
       CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
       c->acc_ready = true;
+      c->plan_ready = true;
     }
     if ((rc = sync(c))) return rc;
     if (out)
@@ -1351,6 +1358,7 @@ int fs_accept(fs_ctx* c, fs_accept_out* out) {
     return FS_OK;
   }
   if (!c->acc_ready) {
+    c->plan_ready = false;
     accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
     CK_LAUNCH(c);
     CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
@@ -1378,6 +1386,14 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
   if (!c->live) return fail(c, FS_ESTATE, "no live round");
   if (!dcs->progress || dcs->n_acc < 1 || dcs->n_acc > c->n_live) return fail(c, FS_ESTATE, "no progress");
   c->acc_ready = false;
+  // the decision fs_accept returned from the verify step: its rank map is
+  // already on the host (prune_plan_kernel), so no device round trip here
+  const TreeRecord* hr = c->h_rec;
+  const bool planned = c->plan_ready && hr->progress && hr->spec_n_pr >= 0 && dcs->n_acc == hr->n_acc &&
+                       (dcs->cont != 0) == (hr->cont != 0) && dcs->x_new == hr->x_new &&
+                       (!dcs->cont || dcs->n_new == hr->n_new_id) &&
+                       !memcmp(dcs->acc_ids, hr->acc_id, sizeof(int32_t) * dcs->n_acc);
+  c->plan_ready = false;
   DecisionIn* di = c->h_dec;
   di->n_acc = dcs->n_acc;
   di->n_new_id = dcs->cont ? dcs->n_new : -1;
@@ -1391,11 +1407,18 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
   // rank map -> host (to re-map the replicated segment schedule)
   static thread_local std::vector<int32_t> hrank;
   hrank.resize(c->cfg.max_live);
-  CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, order), cudaMemcpyDeviceToHost, c->st));
-  CK_CUDA(c, cudaMemcpyAsync(hrank.data(), c->tree.rank, sizeof(int32_t) * c->cfg.max_live,
-                             cudaMemcpyDeviceToHost, c->st));
-  if ((rc = sync(c))) return rc;
-  if (c->h_rec->err) return fail(c, FS_ESTATE, "inconsistent decision");
+  int n_pr_new;
+  if (planned) {
+    memcpy(hrank.data(), hr->spec_rank, sizeof(int32_t) * c->cfg.max_live);
+    n_pr_new = hr->spec_n_pr;
+  } else {
+    CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, order), cudaMemcpyDeviceToHost, c->st));
+    CK_CUDA(c, cudaMemcpyAsync(hrank.data(), c->tree.rank, sizeof(int32_t) * c->cfg.max_live,
+                               cudaMemcpyDeviceToHost, c->st));
+    if ((rc = sync(c))) return rc;
+    if (c->h_rec->err) return fail(c, FS_ESTATE, "inconsistent decision");
+    n_pr_new = c->h_rec->n_pr;
+  }
   const int a = dcs->n_acc;
   const bool cont = dcs->cont != 0;
   // KV-cache pruning of this stage's layers
@@ -1444,7 +1467,7 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
       if (s.e > s.b) nq.push_back(s);
     }
     c->queue.swap(nq);
-    c->n_live = c->h_rec->n_pr;
+    c->n_live = n_pr_new;
     c->l_glo += a;
   } else {
     c->l_glo += a;

@@ -373,6 +373,34 @@ __global__ void __launch_bounds__(TREE_THREADS) prune_kernel(TreeDev t, const De
   }
 }
 
+// The rank map and |I_pr| prune_kernel derives from the decision accept_kernel
+// just recorded (same membership rule: I_acc, plus n_new and its descendants
+// by the ancestor bitset when the round continues), without touching the tree.
+__global__ void __launch_bounds__(TREE_THREADS) prune_plan_kernel(TreeDev t, TreeRecord* rec,
+                                                                  int32_t n_live) {
+  __shared__ unsigned char s_is_acc[MAXLIVE];
+  __shared__ int s_warp[TREE_THREADS / 32 + 1];
+  const int i = threadIdx.x;
+  const bool ok = n_live > 0 && rec->progress && !rec->err;
+  if (i < MAXLIVE) s_is_acc[i] = 0;
+  __syncthreads();
+  const int n_acc = ok ? rec->n_acc : 0;
+  if (i < n_acc) s_is_acc[rec->acc_s[i]] = 1;
+  __syncthreads();
+  const int cont = ok && rec->cont, nn = cont ? rec->n_new_s : 0;
+  bool in_pr = false, in_acc = false;
+  if (ok && i < n_live) {
+    in_acc = s_is_acc[i];
+    if (cont) in_pr = (t.anc[(size_t)i * t.ancw + (nn >> 5)] >> (nn & 31)) & 1u;
+  }
+  const bool ret = in_acc || in_pr;
+  int n_ret, n_pr;
+  const int r = block_excl_count(ret, s_warp, &n_ret);
+  block_excl_count(in_pr, s_warp, &n_pr);
+  if (i < MAXLIVE) rec->spec_rank[i] = (i < n_live && ret) ? r : -1;
+  if (i == 0) rec->spec_n_pr = ok ? n_pr : -1;
+}
+
 // ---------------------------------------------------------------- KV compaction
 // Stable stream-compaction gather over this stage's KV planes:
 // for retained S index i < n_cached, row l_glo+i -> l_glo+rank(i).  rank(i) <= i

@@ -58,6 +58,11 @@ struct TreeRecord {
   int32_t acc_id[MAXLIVE];
   int32_t acc_tok[MAXLIVE];
   int32_t flagged[MAXLIVE];
+  // accept (verify step): the prune rank map this decision implies, computed
+  // ahead so fs_prune_and_compact needs no device round trip when the caller
+  // passes the decision fs_accept returned (prune_plan_kernel)
+  int32_t spec_n_pr;
+  int32_t spec_rank[MAXLIVE];
 };
 
 // Input of the submit kernel (copied host -> device)
