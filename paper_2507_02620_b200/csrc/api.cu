@@ -871,19 +871,17 @@ int head_forward(fs_ctx* c) {
 int stage_forward(fs_ctx* c, bool from_hin) {
   const int d = c->cfg.d_model;
   const int n = c->h_rows->n_rows;
-  if (c->first) {
-    if (c->bf)
-      embed_kernel<bf16><<<FS_MAX_SEG, 256, 0, c->st>>>((const bf16*)c->emb, d, c->d_rows, c->x);
-    else
-      embed_kernel<float><<<FS_MAX_SEG, 256, 0, c->st>>>((const float*)c->emb, d, c->d_rows, c->x);
+  if (c->bf) {  // embedding / received rows -> x, and the first RMSNorm's inputs (one kernel)
+    const bf16* g0 = c->nl > 0 ? (const bf16*)c->lw[0].g1 : (const bf16*)c->gf;
+    const float* src = (!c->first && from_hin) ? c->hin : c->x;
+    norm_prep_kernel<bf16><<<c->npad, 128, 0, c->st>>>(c->first ? (const bf16*)c->emb : nullptr, src, c->x,
+                                                       g0, (bf16*)c->y, c->ssq, d, c->d_rows);
+    CK_LAUNCH(c);
+  } else if (c->first) {
+    embed_kernel<float><<<FS_MAX_SEG, 256, 0, c->st>>>((const float*)c->emb, d, c->d_rows, c->x);
     CK_LAUNCH(c);
   } else if (from_hin) {
     CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)c->cfg.max_seg * d * 4, cudaMemcpyDeviceToDevice, c->st));
-  }
-  if (c->bf) {  // first RMSNorm's inputs: per-128-column sums of squares and x*g (hi/lo)
-    const bf16* g0 = c->nl > 0 ? (const bf16*)c->lw[0].g1 : (const bf16*)c->gf;
-    norm_prep_kernel<<<c->npad, 128, 0, c->st>>>(c->x, g0, (bf16*)c->y, c->ssq, d, c->d_rows);
-    CK_LAUNCH(c);
   }
   for (int l = 0; l < c->nl; l++) {
     int rc = layer_forward(c, l);

@@ -20,27 +20,37 @@ __global__ void embed_kernel(const T* __restrict__ E, int d, const TickRows* row
   for (int k = threadIdx.x; k < d; k += blockDim.x) x[(size_t)m * d + k] = to_f32(E[tok * d + k]);
 }
 
-// First RMSNorm input of a stage's forward (embedding or received rows):
-// per-128-column sums of squares of x [d/128][npad] and z = x*g as the bf16
-// hi/lo B operand [2*npad][d] (RMSNorm applied by linearity in the GEMM).
-__global__ void norm_prep_kernel(const float* __restrict__ x, const bf16* __restrict__ g, bf16* z,
-                                 float* ssq, int d, const TickRows* rows) {
-  const int m = blockIdx.x, np = gridDim.x;
+// First RMSNorm input of a stage's forward: x = the embedding rows (E != null),
+// the received rows (src != x) or x as it is; then per-32-column sums of
+// squares of x [d/32][npad] and z = x*g as the bf16 hi/lo B operand [2*npad][d]
+// (RMSNorm applied by linearity in the GEMM).  Warp w of the CTA covers the
+// 32-column groups 4i + w with coalesced loads; rows >= n_rows give z = 0.
+template <typename TE>
+__global__ void __launch_bounds__(128) norm_prep_kernel(const TE* __restrict__ E, const float* src, float* x,
+                                                        const bf16* __restrict__ g, bf16* z, float* ssq, int d,
+                                                        const TickRows* rows) {
+  const int m = blockIdx.x, np = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool live = m < rows->n_rows;
-  for (int k = threadIdx.x; k < d; k += blockDim.x) {
-    const float v = live ? x[(size_t)m * d + k] * __bfloat162float(g[k]) : 0.f;
-    const bf16 hi = __float2bfloat16_rn(v);
+  const TE* er = (E && live) ? E + (size_t)rows->token[m] * d : nullptr;
+  const float* xs = (E ? x : src) + (size_t)m * d;
+  float* xr = x + (size_t)m * d;
+  const int ng = d / 32;   // d % 32 == 0 (cfg_valid): whole groups, warp-uniform bound
+#pragma unroll 4
+  for (int i = 0; i * 4 + warp < ng; i++) {
+    const int k = i * 128 + warp * 32 + lane;
+    float v = 0.f;
+    if (live) {
+      v = er ? to_f32(er[k]) : xs[k];
+      if (er || src != x) xr[k] = v;
+    }
+    const float gv = v * __bfloat162float(g[k]);
+    const bf16 hi = __float2bfloat16_rn(gv);
     z[(size_t)m * d + k] = hi;
-    z[(size_t)(np + m) * d + k] = __float2bfloat16_rn(v - __bfloat162float(hi));
-  }
-  for (int t = threadIdx.x; t < d / 32; t += blockDim.x) {   // per-32-column partials
-    float s = 0.f;
-    if (live)
-      for (int k = 0; k < 32; k++) {
-        const float v = x[(size_t)m * d + t * 32 + k];
-        s += v * v;
-      }
-    ssq[(size_t)t * np + m] = s;
+    z[(size_t)(np + m) * d + k] = __float2bfloat16_rn(gv - __bfloat162float(hi));
+    float s = v * v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) ssq[(size_t)(i * 4 + warp) * np + m] = s;
   }
 }
 
