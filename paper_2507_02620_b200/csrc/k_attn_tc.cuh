@@ -4,17 +4,18 @@
 // query rows of one kv head share every K/V row, so attention sits at the
 // ridge (256 flop/B at configs[4]) and belongs on the tensor
 // cores.  CTA = (key split, kv head), one CTA per SM:
-//   warp 0     TMA producer: K (and V) tiles of 128 keys, SWIZZLE_128B, 2 stages
+//   warp 0     TMA producer: K and V tiles of 128 keys, SWIZZLE_128B, 2 stages
 //   warp 1     MMA issuer (one thread): S = Q K^T into TMEM; O += P V from TMEM
 //   warps 2..  softmax: 4 warps per 128-row M-tile, one query row per thread
 // TMEM per M-tile: 128 columns S (fp32; P aliases it as bf16 hi | lo halves)
-// and 128 columns O.  Two passes over the split's keys: pass 1 computes the
-// row maxima M (S only), pass 2 recomputes S, writes P = 2^(s - M) as a bf16
-// hi/lo pair (PLO; precision contract R18, as the MHA kernel) or as bf16 (the
-// contract permits it) and accumulates O += P_hi V (+ P_lo V), so O never
-// needs rescaling.  K is read twice (the
-// second time mostly from L2).  The split's unnormalised O and (M, l) go to a
-// workspace that attn_combine_kernel merges in split order (deterministic).
+// and 128 columns O.  One pass with an online softmax: P = 2^(s - M) against
+// a running row maximum M that is raised lazily -- only when a tile's maximum
+// exceeds it by more than 2^8, in which case the thread rescales its O row
+// in TMEM (after the previous P V completed) and its running sum; otherwise
+// P may reach 2^8, exact in fp32 and in the bf16 hi/lo pair (PLO; precision
+// contract R18, as the MHA kernel) or bf16.  The split's unnormalised O and
+// (M, l) go to a workspace that attn_combine_kernel merges in split order
+// (deterministic).
 // Tree visibility (§8(a) a6): context keys [0, ctx_lim[m]) plus
 // ancestors-or-self of the row's node; key tiles below every live row's
 // context limit skip the mask.
@@ -28,7 +29,7 @@ constexpr int TCA_BOX = 128 * 128;       // one SW128 box: 128 rows x 64 bf16 = 
 
 template <int MT2>
 struct TcAttnCfg {
-  static constexpr int THREADS = 64 + 256 * MT2;     // producer, MMA, 8 softmax warps per M-tile
+  static constexpr int THREADS = 64 + 128 * MT2;     // producer, MMA, 4 softmax warps per M-tile
   static constexpr int Q_BYTES = MT2 * 2 * TCA_BOX;   // M-tiles x 2 head-dim boxes
   static constexpr int STAGE_BYTES = 4 * TCA_BOX;     // K (2 boxes) | V (2 boxes)
   static constexpr int NST = 2;
@@ -50,6 +51,11 @@ FS_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
+}
+FS_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 // TMEM -> registers without the wait (the caller waits once for a batch)
 FS_DEV void tmem_ld16_nw(uint32_t taddr, uint32_t* r) {
@@ -105,7 +111,6 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
   int* sCtxMin = reinterpret_cast<int*>(tmem_holder + 1);
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256);
-  float* sHalf = reinterpret_cast<float*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256 + 2048);  // [QR] row max / sum exchange
 
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   const int split = blockIdx.x, kvh = blockIdx.y, nsplit = gridDim.x;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     for (int mi = 0; mi < MT2; mi++) {
       mbar_init(&s_full[mi], 1);
-      mbar_init(&p_full[mi], 256);
+      mbar_init(&p_full[mi], 128);
       mbar_init(&pv_done[mi], 1);
     }
     mbar_init(o_full, 1);
@@ -183,23 +188,19 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   TCA_PROBE(1);
 
   if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer: pass 1 K tiles, pass 2 K + V tiles
-      const uint64_t pol = l2_evict_last_policy();
+    if (lane == 0) {   // ---------------- TMA producer: K + V tiles
+      const uint64_t pol = l2_evict_first_policy();
       int st = 0;
       uint32_t ph = 0;
-      for (int j = 0; j < 2 * T; j++) {
-        const bool pass2 = j >= T;
-        const int t = pass2 ? j - T : j;
+      for (int j = 0; j < T; j++) {
         mbar_wait(&empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&full[st], (pass2 ? 4 : 2) * TCA_BOX);
+        mbar_arrive_expect_tx(&full[st], 4 * TCA_BOX);
         uint8_t* sK = sKV + st * C::STAGE_BYTES;
-        const int y = kvh * a.max_ctx + kbeg + t * TCA_KT;
+        const int y = kvh * a.max_ctx + kbeg + j * TCA_KT;
         tma_load_2d(sK, &tmK, &full[st], 0, y, pol);
         tma_load_2d(sK + TCA_BOX, &tmK, &full[st], 64, y, pol);
-        if (pass2) {
-          tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[st], 0, y, pol);
-          tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[st], 64, y, pol);
-        }
+        tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[st], 0, y, pol);
+        tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[st], 64, y, pol);
         if (++st == C::NST) {
           st = 0;
           ph ^= 1;
@@ -209,9 +210,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {   // ---------------- MMA issuer
-      // Ping-pong over the two M-tiles: after P V of (step j, tile mi) comes
-      // Q K^T of (step j+1, tile mi), so one tile's softmax overlaps the other
-      // tile's MMAs.  Steps j < T are pass 1 (Q K^T only), j >= T pass 2.
+      // Ping-pong over the two M-tiles: after P V of (tile j, M-tile mi) comes
+      // Q K^T of (j+1, mi), so one M-tile's softmax overlaps the other's MMAs.
       constexpr uint32_t idesc_qk = umma_idesc_bf16(128, 128);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);   // B (V) MN-major
       const uint32_t q0 = smem_u32(sQ);
@@ -219,11 +219,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       auto stage_of = [&](int j) { return j % C::NST; };
       auto issue_qk = [&](int j, int mi) {
         if (mi == 0) mbar_wait(&full[stage_of(j)], (uint32_t)((j / C::NST) & 1));
-        // the S / P columns of tile mi must be free
-        if (j > 0) {
-          if (j - 1 < T) mbar_wait(&p_full[mi], (uint32_t)((j - 1) & 1));   // softmax read S
-          else mbar_wait(&pv_done[mi], (uint32_t)((j - 1 - T) & 1));        // P V read P
-        }
+        // the S / P columns of M-tile mi are free once P V of tile j-1 read P
+        if (j > 0) mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));
         tc_fence_after();
         const uint32_t k0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES);
         const uint32_t tS = tmem + (uint32_t)(mi * 256);
@@ -236,26 +233,25 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
         umma_commit(&s_full[mi]);
       };
       auto issue_pv = [&](int j, int mi) {
-        mbar_wait(&p_full[mi], (uint32_t)(j & 1));   // P of this step written
+        mbar_wait(&p_full[mi], (uint32_t)(j & 1));   // P of this tile written (and O rescaled)
         tc_fence_after();
         const uint32_t v0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES) + 2 * TCA_BOX;
         const uint32_t tS = tmem + (uint32_t)(mi * 256), tO = tS + 128;
-        const int t = j - T;
 #pragma unroll
         for (int ks = 0; ks < 8; ks++) {
           const uint64_t bd = umma_sdesc_sw128_mn(v0 + ks * 2048, TCA_BOX, 1024);
           // keys 16ks.. live in the column half ks / 4: P_hi at +0, P_lo at +32
           const uint32_t pa = tS + (uint32_t)((ks >> 2) * 64 + (ks & 3) * 8);
-          umma_bf16_tmemA(tO, pa, bd, idesc_pv, (t > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_tmemA(tO, pa, bd, idesc_pv, (j > 0 || ks > 0) ? 1u : 0u);
           if constexpr (PLO) umma_bf16_tmemA(tO, pa + 32, bd, idesc_pv, 1u);
         }
         umma_commit(&pv_done[mi]);
       };
       for (int mi = 0; mi < MT2; mi++) issue_qk(0, mi);
-      for (int j = 0; j < 2 * T; j++) {
+      for (int j = 0; j < T; j++) {
         for (int mi = 0; mi < MT2; mi++) {
-          if (j >= T) issue_pv(j, mi);
-          if (j + 1 < 2 * T) issue_qk(j + 1, mi);
+          issue_pv(j, mi);
+          if (j + 1 < T) issue_qk(j + 1, mi);
         }
         umma_commit(&empty[stage_of(j)]);   // stage j's K / V reads are all issued
       }
@@ -263,9 +259,9 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ---------------- softmax: two threads per query row (TMEM lane quarter
-    // warp % 4, key / column half hh); each writes P only into its own half
-    const int wi = warp - 2, mi = wi >> 3, q = warp & 3, hh = (wi >> 2) & 1;
+    // ---------------- softmax: one thread per query row (TMEM lane quarter
+    // warp % 4); the running maximum M is in raw-score units
+    const int wi = warp - 2, mi = wi >> 2, q = warp & 3;
     const int rr = q * 32 + lane, r = mi * 128 + rr;
     const int m = r % a.npad;
     const bool live = m < n_rows;
@@ -273,121 +269,142 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     const int slr = live ? rows->sidx[m] : -1;
     const int l_glo = rows->l_glo;
     const int ctx_min = *sCtxMin;
-    const uint32_t tS = tmem + (uint32_t)(mi * 256) + ((uint32_t)(q * 32) << 16) + (uint32_t)(hh * 64);
+    const float sc = a.scale_log2;
+    const uint32_t tS = tmem + (uint32_t)(mi * 256) + ((uint32_t)(q * 32) << 16), tO = tS + 128;
     float M = -INFINITY, L = 0.f;
-    for (int j = 0; j < 2 * T; j++) {
-      const bool pass2 = j >= T;
-      const int t = pass2 ? j - T : j;
-      if (j == T) {   // pass boundary: row max of both halves
-        if (hh == 1) sHalf[r] = M;
-        named_bar_sync(1 + mi, 256);
-        if (hh == 0) M = fmaxf(M, sHalf[r]);
-        named_bar_sync(1 + mi, 256);
-        if (hh == 0) sHalf[r] = M;
-        named_bar_sync(1 + mi, 256);
-        if (hh == 1) M = sHalf[r];
-      }
+    for (int j = 0; j < T; j++) {
       mbar_wait(&s_full[mi], j & 1);
       tc_fence_after();
       if (j == 0) TCA_PROBE(2);
-      if (j == T) TCA_PROBE(4);
-      if (j == 2 * T - 1) TCA_PROBE(6);
-      float s[64];
-#pragma unroll
-      for (int c = 0; c < 4; c++) tmem_ld16_nw(tS + c * 16, reinterpret_cast<uint32_t*>(s + c * 16));
-      tmem_ld_wait();
-      if (!pass2) {   // S is in registers: the next Q K^T may overwrite it
-        tc_fence_before();
-        mbar_arrive(&p_full[mi]);
-      }
-      const int key0 = kbeg + t * TCA_KT + hh * 64;
+      if (j == T - 1) TCA_PROBE(6);
+      const int key0 = kbeg + j * TCA_KT;
       // raw scores; invisible keys -> -inf (ex2 maps them to 0 below)
-      if (!(key0 + 64 <= min(kend, ctx_min))) {
+      const bool need_mask = !(key0 + TCA_KT <= min(kend, ctx_min));
+      auto mask16 = [&](float* t, int kb) {
 #pragma unroll
-        for (int i = 0; i < 64; i++) {
-          const int key = key0 + i;
+        for (int i = 0; i < 16; i++) {
+          const int key = kb + i;
           bool vis = live && key < kend;
           if (vis && key >= ctxr) {
             const int aa = key - l_glo;
             vis = slr >= 0 && aa >= 0 && aa < a.max_live &&
                   ((sAnc[m * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
           }
-          if (!vis) s[i] = -INFINITY;
+          if (!vis) t[i] = -INFINITY;
         }
-      }
-      if (!pass2) {
-        float mx[4] = {M, -INFINITY, -INFINITY, -INFINITY};   // independent chains
+      };
+      // pass A: the tile's row maximum (S re-read from TMEM in pass B, which
+      // keeps the register footprint at one 64-key half)
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};   // independent chains
 #pragma unroll
-        for (int i = 0; i < 64; i++) mx[i & 3] = fmaxf(mx[i & 3], s[i]);
-        M = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-        if (j == T - 1) TCA_PROBE(3);
+      for (int c = 0; c < 8; c += 2) {
+        float t[32];
+        tmem_ld16_nw(tS + c * 16, reinterpret_cast<uint32_t*>(t));
+        tmem_ld16_nw(tS + c * 16 + 16, reinterpret_cast<uint32_t*>(t + 16));
+        tmem_ld_wait();
+        if (need_mask) {
+          mask16(t, key0 + c * 16);
+          mask16(t + 16, key0 + c * 16 + 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i++) mx[i & 3] = fmaxf(mx[i & 3], t[i]);
+      }
+      const float Mn = fmaxf(M, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));
+      if (j == 0) {
+        M = Mn;
       } else {
-        // p = 2^(s * scale - M * scale): one FFMA + ex2 per element (the scale
-        // is positive, so the raw-score max is the scaled max); a row with no
-        // visible key has M = -inf and keeps p = 0
-        const float sc = a.scale_log2;
-        const float nm = (M == -INFINITY) ? 0.f : -M * sc;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        // lazy rescale: only when the tile maximum exceeds M by more than 2^8
+        const bool resc = Mn != -INFINITY && (M == -INFINITY || (Mn - M) * sc > 8.f);
+        if (__any_sync(0xffffffffu, resc)) {   // tcgen05.ld / st are warp-collective
+          mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));   // O holds tiles < j
+          tc_fence_after();
+          const float f = resc ? ((M == -INFINITY) ? 0.f : ex2_approx((M - Mn) * sc)) : 1.f;
 #pragma unroll
-        for (int i = 0; i < 64; i++) {
-          const float p = ex2_approx(fmaf(s[i], sc, nm));
-          s[i] = p;
-          ls[i & 3] += p;
-        }
-        L += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-        // P_hi -> this half's columns [0, 32); P_lo = p - float(P_hi) -> [32, 64)
-        // (hi halves unpacked with integer ops, no second rounding)
-        uint32_t pk[32], pl[32];
+          for (int c = 0; c < 4; c++) {
+            uint32_t o[32];
+            tmem_ld16_nw(tO + c * 32, o);
+            tmem_ld16_nw(tO + c * 32 + 16, o + 16);
+            tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
-          const float x0 = s[2 * i], x1 = s[2 * i + 1];
-          const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(&hb);
-          pk[i] = u;
-          if constexpr (PLO)
-            pl[i] = pack_bf16(x0 - __uint_as_float(u << 16), x1 - __uint_as_float(u & 0xFFFF0000u));
+            for (int i = 0; i < 32; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+            tmem_st32(tO + c * 32, o);
+          }
+          tmem_st_wait();
+          if (resc) {
+            L *= f;
+            M = Mn;
+          }
         }
-        tmem_st32(tS, pk);
-        if constexpr (PLO) tmem_st32(tS + 32, pl);
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&p_full[mi]);
-        if (j == T) TCA_PROBE(5);
       }
+      // p = 2^(s * scale - M * scale): one FFMA + ex2 per element (the scale
+      // is positive); a row with no visible key so far has M = -inf, p = 0
+      const float nm = (M == -INFINITY) ? 0.f : -M * sc;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        // pass B, one 64-key half at a time: its P columns alias only its own S
+        // columns, so the half is fully read before any of them is written
+        float s[64];
+#pragma unroll
+        for (int c = 0; c < 4; c++) tmem_ld16_nw(tS + hh * 64 + c * 16, reinterpret_cast<uint32_t*>(s + c * 16));
+        tmem_ld_wait();
+        if (need_mask)
+#pragma unroll
+          for (int c = 0; c < 4; c++) mask16(s + c * 16, key0 + hh * 64 + c * 16);
+#pragma unroll
+        for (int c16 = 0; c16 < 4; c16++) {   // 16 keys: 8 packed hi columns (+ 8 lo columns)
+          uint32_t pk[8], pl[8];
+#pragma unroll
+          for (int i = 0; i < 8; i++) {
+            const int k0 = c16 * 16 + 2 * i;
+            const float x0 = ex2_approx(fmaf(s[k0], sc, nm)), x1 = ex2_approx(fmaf(s[k0 + 1], sc, nm));
+            ls[i & 3] += x0 + x1;
+            // P_hi -> columns [0, 32) of the half; P_lo = p - float(P_hi) -> [32, 64)
+            // (hi halves unpacked with integer ops, no second rounding)
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+            const uint32_t u = *reinterpret_cast<const uint32_t*>(&hb);
+            pk[i] = u;
+            if constexpr (PLO)
+              pl[i] = pack_bf16(x0 - __uint_as_float(u << 16), x1 - __uint_as_float(u & 0xFFFF0000u));
+          }
+          tmem_st8(tS + hh * 64 + c16 * 8, pk);
+          if constexpr (PLO) tmem_st8(tS + hh * 64 + 32 + c16 * 8, pl);
+        }
+      }
+      L += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[mi]);
     }
-    // ---------------- unnormalised O half-row and (M, l) of this split
+    // ---------------- unnormalised O row and (M, l) of this split
     TCA_PROBE(7);
-    if (hh == 1) sHalf[r] = L;
-    named_bar_sync(1 + mi, 256);
-    if (hh == 0) L += sHalf[r];
     mbar_wait(o_full, 0);
     tc_fence_after();
     TCA_PROBE(8);
-    float o[64];
-#pragma unroll
-    for (int c = 0; c < 4; c++)
-      tmem_ld16_nw(tS - (uint32_t)(hh * 64) + 128 + (uint32_t)(hh * 64) + c * 16, reinterpret_cast<uint32_t*>(o + c * 16));
-    tmem_ld_wait();
-    // every MMA has completed: the Q / K / V buffers stage the warp's 32 half
-    // rows so that the workspace write is coalesced (a warp's rows r are
-    // consecutive); rows padded to 68 floats keep the 16-byte stores at 4 wavefronts
-    constexpr int SLD = 64 + 4;
+    // every MMA has completed: the Q / K / V buffers stage the warp's 32 rows
+    // so that the workspace write is coalesced (a warp's rows r are
+    // consecutive); rows padded to 132 floats keep the 16-byte stores at 4 wavefronts
+    constexpr int SLD = 128 + 4;
     float* stg = reinterpret_cast<float*>(smem) + (size_t)wi * 32 * SLD;
 #pragma unroll
-    for (int i = 0; i < 16; i++)
-      *reinterpret_cast<float4*>(stg + lane * SLD + 4 * i) = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    for (int c = 0; c < 4; c++) {
+      float o[32];
+      tmem_ld16_nw(tO + c * 32, reinterpret_cast<uint32_t*>(o));
+      tmem_ld16_nw(tO + c * 32 + 16, reinterpret_cast<uint32_t*>(o + 16));
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        *reinterpret_cast<float4*>(stg + lane * SLD + c * 32 + 4 * i) =
+            make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    }
     __syncwarp();
-    float* dst = ws_o + (size_t)(r - lane) * ATT_HD + hh * 64;
+    float* dst = ws_o + (size_t)(r - lane) * ATT_HD;
 #pragma unroll 8
-    for (int i = 0; i < 16; i++) {   // 32 rows x 16 float4: lane -> (row 2i + lane/16, chunk lane%16)
-      const int row = 2 * i + (lane >> 4), ch = lane & 15;
-      *reinterpret_cast<float4*>(dst + (size_t)row * ATT_HD + 4 * ch) =
-          *reinterpret_cast<const float4*>(stg + row * SLD + 4 * ch);
-    }
-    if (hh == 0) {
-      ws_ml[r * 2] = (M == -INFINITY) ? -INFINITY : M * a.scale_log2;   // log2 units, as the combine expects
-      ws_ml[r * 2 + 1] = L;
-    }
+    for (int row = 0; row < 32; row++)   // one 512-byte row per instruction
+      *reinterpret_cast<float4*>(dst + (size_t)row * ATT_HD + 4 * lane) =
+          *reinterpret_cast<const float4*>(stg + row * SLD + 4 * lane);
+    ws_ml[r * 2] = (M == -INFINITY) ? -INFINITY : M * sc;   // log2 units, as the combine expects
+    ws_ml[r * 2 + 1] = L;
     TCA_PROBE(9);
   }
   tc_fence_before();
