@@ -735,7 +735,13 @@ int launch_attention(fs_ctx* c, int l) {
       }
       prof_end(c, api);
       CK_LAUNCH(c);
-      attn_combine_kernel<<<dim3(np, H), ATT_HD, 0, c->st>>>(a, (bf16*)c->att, 1, nsplit);
+      cudaLaunchConfig_t cc = {};
+      cc.gridDim = dim3(np, H);
+      cc.blockDim = dim3(ATT_HD);
+      cc.stream = c->st;
+      cc.attrs = at;   // programmatic dependent launch
+      cc.numAttrs = 1;
+      cudaLaunchKernelEx(&cc, attn_combine_kernel, a, (bf16*)c->att, 1, nsplit);
       CK_LAUNCH(c);
       return FS_OK;
     }

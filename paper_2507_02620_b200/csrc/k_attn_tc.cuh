@@ -171,6 +171,23 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // context K/V tiles (below the first slot this tick writes) do not depend on
+  // the QKV GEMM: the producer streams the first stages before the dependency
+  int npre = 0;
+  if (tid == 0) {
+    const int first_written = rows->slot[0];
+    const uint64_t pol = l2_evict_first_policy();
+    while (npre < min(T, C::NST) && kbeg + (npre + 1) * TCA_KT <= first_written) {
+      mbar_arrive_expect_tx(&full[npre], 4 * TCA_BOX);
+      uint8_t* sK = sKV + npre * C::STAGE_BYTES;
+      const int y = kvh * a.max_ctx + kbeg + npre * TCA_KT;
+      tma_load_2d(sK, &tmK, &full[npre], 0, y, pol);
+      tma_load_2d(sK + TCA_BOX, &tmK, &full[npre], 64, y, pol);
+      tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[npre], 0, y, pol);
+      tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[npre], 64, y, pol);
+      npre++;
+    }
+  }
   // dependents may launch only now: this CTA already holds its TMEM columns
   pdl_trigger();
   pdl_wait();   // Q and this tick's K/V rows come from the QKV GEMM
@@ -190,9 +207,9 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {   // ---------------- TMA producer: K + V tiles
       const uint64_t pol = l2_evict_first_policy();
-      int st = 0;
-      uint32_t ph = 0;
-      for (int j = 0; j < T; j++) {
+      int st = npre % C::NST;
+      uint32_t ph = (uint32_t)((npre / C::NST) & 1);
+      for (int j = npre; j < T; j++) {
         mbar_wait(&empty[st], ph ^ 1);
         mbar_arrive_expect_tx(&full[st], 4 * TCA_BOX);
         uint8_t* sK = sKV + st * C::STAGE_BYTES;

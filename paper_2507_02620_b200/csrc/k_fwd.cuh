@@ -405,23 +405,46 @@ __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {
 // grid (npad, H), block 128 (one thread per head-dim element)
 __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks, int n_parts_fixed = 0) {
   const int m = blockIdx.x, h = blockIdx.y;
+  pdl_trigger();   // the next kernel streams its weights meanwhile
   if (m >= a.rows->n_rows) return;
   const int n_parts = n_parts_fixed > 0 ? n_parts_fixed : (a.rows->n_keys + ATT_KC - 1) / ATT_KC * ks;
   const int G = a.H / a.Hkv;
   const int kvh = h / G, g = h % G;
   const int QR = G * a.npad;
   const int r = g * a.npad + m;
-  float M = -INFINITY;
-  for (int c = 0; c < n_parts; c++)
-    M = fmaxf(M, a.ws_ml[(((size_t)c * a.Hkv + kvh) * QR + r) * 2]);
-  float L = 0.f, acc = 0.f;
   const int j = threadIdx.x;
-  for (int c = 0; c < n_parts; c++) {
-    const float* ml = a.ws_ml + (((size_t)c * a.Hkv + kvh) * QR + r) * 2;
-    if (ml[0] == -INFINITY) continue;
-    const float w = exp2f(ml[0] - M);
-    L += ml[1] * w;
-    acc += a.ws_o[(((size_t)c * a.Hkv + kvh) * QR + r) * ATT_HD + j] * w;
+  pdl_wait();      // the split partials come from the attention kernel
+  // loads of 8 splits in flight together; accumulation in split order (deterministic)
+  constexpr int B = 8;
+  float M = -INFINITY;
+  for (int c0 = 0; c0 < n_parts; c0 += B) {
+    float mm[B];
+#pragma unroll
+    for (int i = 0; i < B; i++)
+      mm[i] = (c0 + i < n_parts) ? a.ws_ml[(((size_t)(c0 + i) * a.Hkv + kvh) * QR + r) * 2] : -INFINITY;
+#pragma unroll
+    for (int i = 0; i < B; i++) M = fmaxf(M, mm[i]);
+  }
+  float L = 0.f, acc = 0.f;
+  for (int c0 = 0; c0 < n_parts; c0 += B) {
+    float mm[B], ll[B], oo[B];
+#pragma unroll
+    for (int i = 0; i < B; i++) {
+      mm[i] = -INFINITY;
+      if (c0 + i < n_parts) {
+        const size_t base = ((size_t)(c0 + i) * a.Hkv + kvh) * QR + r;
+        mm[i] = a.ws_ml[base * 2];
+        ll[i] = a.ws_ml[base * 2 + 1];
+        oo[i] = a.ws_o[base * ATT_HD + j];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < B; i++) {
+      if (mm[i] == -INFINITY) continue;
+      const float w = exp2f(mm[i] - M);
+      L += ll[i] * w;
+      acc += oo[i] * w;
+    }
   }
   const float o = acc / L;
   const bf16 hi = __float2bfloat16_rn(o);
