@@ -295,6 +295,13 @@ def ours(args):
         gp.set_profiling(False)
         prof = gp.get_profile()
         prof["step_ms"] = step_ms
+        # per-launch GEMM time with launches back to back (programmatic overlap
+        # between consecutive launches as in the step; the event pairs above
+        # serialise every launch): tick rows of a full 16-row prefill chunk
+        gp.fs_set_prefix(prefix, F.FS_PREFILL)
+        if rank == 0:
+            prof["b2b"] = gemm_back_to_back(gp, last=(P == 1))
+            prof["attn_b2b"] = min((gp.bench_kernel(5, 20) for _ in range(3)), key=lambda x: x[0])
 
     if rank != 0:
         return
@@ -336,19 +343,34 @@ def ours(args):
     if prof:
         g_ms = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
         g_bytes = prof["gemm_bytes"] / max(prof["gemm_launches"], 1)
-        ach = g_bytes / (g_ms / 1e3) / 1e9
+        ach_ev = g_bytes / (g_ms / 1e3) / 1e9
+        b2b = prof["b2b"]
+        n_l = shape.n_layers // P
+        cnt = {k: (1 if k == "head" else n_l) for k in b2b}
+        b_bytes = sum(cnt[k] * b2b[k]["bytes"] for k in b2b)
+        b_us = sum(cnt[k] * b2b[k]["us"] for k in b2b)
+        ach = b_bytes / (b_us * 1e-6) / 1e9
         rec["roofline"] = {
-            "kernel": "gemm_tc_kernel (tcgen05 weight-streaming GEMM, all layers + head)",
+            "kernel": "gemm_cluster_kernel / gemm_tc_kernel (tcgen05 weight-streaming GEMMs, all layers + head)",
             "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(ach / hbm, 4), "traffic": ncu_traffic(g_bytes), "peak_source": peak_src,
+            "per_kernel": {k: {"us": round(v["us"], 2), "bytes": v["bytes"],
+                               "GB/s": round(v["bytes"] / v["us"] / 1e3, 1)} for k, v in b2b.items()},
+            "event_pairs": {"achieved": round(ach_ev, 1), "frac": round(ach_ev / hbm, 4),
+                            "note": "event pair around every launch of a profiled round (serialises launches)"},
             "launches_per_step": prof["gemm_launches"],
-            "share_of_step": round(prof["gemm_ms"] / prof["step_ms"], 4),
+            "share_of_step": round(min(1.0, b_us * 1e-3 * (ticks / K) / (dev_ms / K)), 4),
             "attention": {
-                "achieved": round(prof["attn_bytes"] / max(prof["attn_ms"], 1e-9) / 1e6, 1),
+                "achieved": round(prof["attn_b2b"][1] / prof["attn_b2b"][0] / 1e3, 1),
+                "us_per_layer": round(prof["attn_b2b"][0], 2),
+                "frac": round(prof["attn_b2b"][1] / prof["attn_b2b"][0] / 1e3 / hbm, 4),
                 "unit": "GB/s", "launches_per_step": prof["attn_launches"],
+                "event_pairs_achieved": round(prof["attn_bytes"] / max(prof["attn_ms"], 1e-9) / 1e6, 1),
                 "share_of_step": round(prof["attn_ms"] / prof["step_ms"], 4)},
-            "measured": "CUDA event pair around every GEMM/attention launch over one profiled "
-                        "round after the timed region (same workload)",
+            "measured": "GEMM: per launch = CUDA events around 20 back-to-back launches of each "
+                        "weight GEMM (layer 0 of this stage, real epilogues, 16-row tick), weighted "
+                        "by launches per tick; bytes = weights (dominant). Attention: 20 back-to-back launches "
+                        "of layer 0's attention at the bench shape (1024-token context, 16 rows)",
         }
     if P == 1 and not args.no_cpu_baseline:
         rec["cpu_baseline"] = cpu_baseline(shape, trees[0], prefix, ranks, tokens / K, ticks / K,
@@ -373,6 +395,21 @@ def ncu_traffic(alg_bytes_per_launch):
         return round(alg_bytes_per_launch * ratio)
     except Exception:
         return None
+
+
+def gemm_back_to_back(gp, last):
+    """Per-launch time of each weight GEMM class (fs_bench_kernel kinds 0-4:
+    QKV, O, gate/up, down, head) over 20 back-to-back launches, best of 3."""
+    out = {}
+    for k, name in ((0, "qkv"), (1, "o"), (2, "gate_up"), (3, "down"), (4, "head")):
+        if name == "head" and not last:
+            continue
+        best = None
+        for _ in range(3):
+            us, by = gp.bench_kernel(k, 20)
+            best = (us, by) if best is None or us < best[0] else best
+        out[name] = {"us": best[0], "bytes": best[1]}
+    return out
 
 
 def attention_long_context(hbm):

@@ -1750,15 +1750,18 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
   GemmEpi e = base_epi(c);
   const GemmOp* g = nullptr;
   switch (kind) {
-    case 0: g = &w.qkv; e.mode = EPI_QKV; e.bias = (const bf16*)w.bqkv; e.q_out = (bf16*)c->q;
+    case 0: e = norm_input(c); g = &w.qkv; e.mode = EPI_QKV; e.bias = (const bf16*)w.bqkv; e.q_out = (bf16*)c->q;
             e.k_cache = (bf16*)kv_plane(c, 0, 0); e.v_cache = (bf16*)kv_plane(c, 0, 1); break;
-    case 1: g = &w.o; e.mode = EPI_STORE; e.out = c->x; e.ldo = 0; break;
-    case 2: g = &w.gu; e.mode = EPI_GLU; e.act = (bf16*)c->act; break;
-    case 3: g = &w.dn; e.mode = EPI_STORE; e.out = c->x; e.ldo = 0; break;
-    case 4: g = &c->head; e.mode = EPI_HEAD; e.head_part = c->head_part; break;
+    // O / down: the real residual epilogue (x += ., next norm operand, sums of
+    // squares); x drifts over the iterations (timing only)
+    case 1: g = &w.o; e.mode = EPI_RESID; e.x = c->x; e.ssq_out = c->ssq;
+            e.z_gain = (const bf16*)w.g2; e.z_out = (bf16*)c->y; break;
+    case 2: e = norm_input(c); g = &w.gu; e.mode = EPI_GLU; e.act = (bf16*)c->act; break;
+    case 3: g = &w.dn; e.mode = EPI_RESID; e.x = c->x; e.ssq_out = c->ssq;
+            e.z_gain = (const bf16*)w.g1; e.z_out = (bf16*)c->y; break;
+    case 4: e = norm_input(c); g = &c->head; e.mode = EPI_HEAD; e.head_part = c->head_part; break;
     default: break;
   }
-  // EPI_STORE with ldo 0 writes row 0 only: benchmark without touching x rows
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
