@@ -465,7 +465,8 @@ __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks, int n_parts_f
 constexpr int ATT_SUB = 64;   // keys per sub-chunk
 constexpr int ATT_NBUF = 3;   // sub-chunk ring depth
 constexpr int ATT_MAXQR = 32;
-constexpr int ATT_SO_LD = ATT_HD + 4;   // padded row of the key-warp state scratch
+constexpr int ATT_SO_LD = ATT_HD + 8;   // padded row of the key-warp state scratch (float2
+                                        // stores of a half-warp: 4 rows x 8 banks, conflict-free)
 
 struct AttnMhaArgs {
   AttnArgs a;
@@ -650,9 +651,11 @@ FS_DEV void mha_ks_merge(MhaWarp<KPW>& w, const AttnArgs& a, float* so, float* s
     }
   }
   named_bar_sync(bar_id, 128);
-  // 8 threads per row, 16 head dims (4 x float4) each; KS <= 4 unrolled
+  // 8 threads per row, 16 head dims each as 4 float4 interleaved at a 32-float
+  // stride (a quarter-warp's 8 float4 cover 32 consecutive banks: no conflicts);
+  // KS <= 4 unrolled
   for (int r = tid >> 3; r < QR; r += 16) {
-    const int m2 = r / 16, r16 = r % 16, d0 = (tid & 7) * 16;
+    const int m2 = r / 16, r16 = r % 16, d0 = (tid & 7) * 4;
     float mm[KS], M = -INFINITY;
 #pragma unroll
     for (int k2 = 0; k2 < KS; k2++) {
@@ -668,19 +671,19 @@ FS_DEV void mha_ks_merge(MhaWarp<KPW>& w, const AttnArgs& a, float* so, float* s
       const int ww = m2 + MT * k2;
       const float wt = (mm[k2] == -INFINITY) ? 0.f : exp2f(mm[k2] - M);
       L += sml[(ww * 16 + r16) * 2 + 1] * wt;
-      const float4* src = reinterpret_cast<const float4*>(so + ((size_t)ww * 16 + r16) * ATT_SO_LD + d0);
+      const float* src = so + ((size_t)ww * 16 + r16) * ATT_SO_LD + d0;
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const float4 o = src[u];
+        const float4 o = *reinterpret_cast<const float4*>(src + 32 * u);
         acc[u].x += o.x * wt;
         acc[u].y += o.y * wt;
         acc[u].z += o.z * wt;
         acc[u].w += o.w * wt;
       }
     }
-    float4* dst = reinterpret_cast<float4*>(sPart + r * ATT_HD + d0);
+    float* dst = sPart + r * ATT_HD + d0;
 #pragma unroll
-    for (int u = 0; u < 4; u++) dst[u] = acc[u];
+    for (int u = 0; u < 4; u++) *reinterpret_cast<float4*>(dst + 32 * u) = acc[u];
     if ((tid & 7) == 0) {
       sPml[r * 2] = M;
       sPml[r * 2 + 1] = L;
