@@ -628,6 +628,7 @@ int launch_attention(fs_ctx* c, int l) {
     a.npad = np;
     a.n_chunk_cap = c->att_chunk_cap;
     a.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)hd));
+    a.resc_log2 = getenv("FS_TCA_RESCALE") ? (float)atof(getenv("FS_TCA_RESCALE")) : 8.f;
     a.dbg = c->att_dbg;
     a.dbg_ends = c->att_dbg_ends;
     if (c->tl_buf) {

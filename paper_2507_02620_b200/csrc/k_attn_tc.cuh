@@ -330,8 +330,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       if (j == 0) {
         M = Mn;
       } else {
-        // lazy rescale: only when the tile maximum exceeds M by more than 2^8
-        const bool resc = Mn != -INFINITY && (M == -INFINITY || (Mn - M) * sc > 8.f);
+        // lazy rescale: only when the tile maximum exceeds M by more than 2^resc_log2 (8)
+        const bool resc = Mn != -INFINITY && (M == -INFINITY || (Mn - M) * sc > a.resc_log2);
         if (__any_sync(0xffffffffu, resc)) {   // tcgen05.ld / st are warp-collective
           mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));   // O holds tiles < j
           tc_fence_after();

@@ -212,6 +212,8 @@ struct AttnArgs {
   float* ws_ml;         // [n_chunk_cap][Hkv][QR][2]
   int ancw, max_live, H, Hkv, max_ctx, npad, n_chunk_cap;
   float scale_log2;     // log2(e) / sqrt(hd)
+  float resc_log2;      // GQA online softmax: raise the running max when a tile exceeds it by more
+                        // than 2^resc_log2 (8; FS_TCA_RESCALE overrides, 0 = at every increase: tests)
   unsigned long long* dbg;  // optional phase timestamps [cta][16] (diagnostics)
   int dbg_ends;             // diagnostics: record only the first and last probe
 };

@@ -73,3 +73,12 @@ def test_72b_layers_gqa_bias_32row_segments_long_context():
     M = 8 x 32 rows), q/k/v bias, 32-row segments (UMMA N = 64), 16K-token
     synthetic-KV context (130 attention chunks), 256-node trees."""
     _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
+
+
+def test_72b_gqa_online_softmax_rescale_path(monkeypatch):
+    """The GQA kernel's lazy online-softmax rescale (running max raised, O rows
+    rescaled in TMEM) normally triggers only on a > 2^8 jump of the row max;
+    threshold 0 forces it at every increase of the max, so the path is checked
+    against the oracle on the configs[4] per-layer shapes."""
+    monkeypatch.setenv("FS_TCA_RESCALE", "0")
+    _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
