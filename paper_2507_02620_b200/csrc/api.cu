@@ -264,9 +264,13 @@ void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const ch
   g.sh.n_tiles = (n_out + 127) / 128;
   g.sh.units = g.sh.n_tiles * g.sh.kb_total;
   g.sh.late_trigger = getenv("FS_LATE_TRIGGER") ? 1 : 0;
-  // stream-K: one CTA per SM (two per SM measured 3.15 vs 2.92 ms per 7B tick:
+  // Many tiles, gemm_tc_kernel: one CTA per output tile when all tiles fit one
+  // wave (no split-K, no fix-up; 7B gate/up: 172 CTAs, tick 2.88 -> 2.79 ms),
+  // else stream-K over one CTA per SM (two per SM measured 3.15 vs 2.92 ms:
   // the next GEMM's CTAs then find no free slot to prefetch into)
   g.grid = std::min(n_sms, g.sh.units);
+  if (g.sh.n_tiles > n_sms && g.sh.n_tiles <= ctas_per_sm * n_sms && !getenv("FS_NO_TILE_GRID"))
+    g.grid = g.sh.n_tiles;
   // Few output tiles: tile-aligned cluster split-K with S CTAs per tile.  Two
   // CTAs fit per SM (NT 16): S = the largest power of two keeping the grid in
   // one wave of 2 x SMs slots; otherwise S = floor(SMs / tiles).  Many tiles:
