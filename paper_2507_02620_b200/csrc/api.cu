@@ -683,6 +683,7 @@ int launch_attention(fs_ctx* c, int l) {
           }
           if (nclu >= Hkv) break;
         }
+        if (getenv("FS_ATT_NSPLIT")) ns = std::max(1, std::min(ns, atoi(getenv("FS_ATT_NSPLIT"))));
         c->att_nsplit[MT] = ns;
       }
       const int nsplit = c->att_nsplit[MT];
