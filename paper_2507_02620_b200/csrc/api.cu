@@ -410,7 +410,7 @@ bool setup_ctx(fs_ctx* c, const fs_config* f) {
   c->bf = f->bf16 != 0;
   c->esz = c->bf ? 2 : 4;
   c->npad = npad_of(f->max_seg);
-  c->gemm_ctas = c->npad <= 16 ? 2 : 1;   // GemmCfg<NT>::MIN_CTAS
+  c->gemm_ctas = c->npad <= 16 ? GemmCfg<16>::MIN_CTAS : 1;
   c->ancw = f->max_live / 32;
   return true;
 }

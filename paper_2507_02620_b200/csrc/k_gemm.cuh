@@ -86,6 +86,12 @@ struct GemmEpi {
 // rows [0,NT) and [NT,2NT) of the B tile), so UMMA N = 2*NT and the epilogue
 // adds the two accumulator halves: the GEMM sees ~16-bit-mantissa activations
 // at no HBM cost (the weights dominate the bytes).
+#ifndef FS_GEMM_STAGES16
+#define FS_GEMM_STAGES16 5
+#endif
+#ifndef FS_GEMM_CTAS16
+#define FS_GEMM_CTAS16 2
+#endif
 template <int NT>
 struct GemmCfg {
   static constexpr int BN = 2 * NT;                      // UMMA N
@@ -94,8 +100,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // NT=16: 5 stages -> ~110 KB, two CTAs per SM (the next GEMM's CTA starts
   // streaming its weights while this one drains: early PDL trigger)
-  static constexpr int STAGES = NT <= 16 ? 5 : (NT <= 32 ? 4 : 3);
-  static constexpr int MIN_CTAS = NT <= 16 ? 2 : 1;   // ~110 KB: two CTAs per SM
+  static constexpr int STAGES = NT <= 16 ? FS_GEMM_STAGES16 : (NT <= 32 ? 4 : 3);
+  static constexpr int MIN_CTAS = NT <= 16 ? FS_GEMM_CTAS16 : 1;   // ~110 KB: two CTAs per SM
   // two accumulator buffers (segment s uses buffer s&1) so the MMA of the next
   // tile segment never waits for the epilogue of the previous one
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
