@@ -1303,30 +1303,32 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     c->h_rows->n_keys = c->l_glo + cur.e;
     if ((rc = tick_forward(c))) return rc;
   }
-  // stage transport: p -> p+1 hidden rows (fp32), NCCL over NVLink
+  // stage transport: p -> p+1 hidden rows (fp32), NCCL over NVLink, grouped
+  // with the broadcast of the last stage's row results (one NCCL launch per tick)
+  const Seg outseg = c->slot[P - 1];
+  const bool out_rows = outseg.valid() && outseg.n() > 0;
   if (P > 1) {
     const Seg prev = c->slot[p > 0 ? p - 1 : 0];
     const bool recv = p > 0 && prev.valid() && prev.n() > 0;
     const bool send = !c->last && has;
-    if (recv || send) {
+    if (recv || send || out_rows) {
       CK_NCCL(c, ncclGroupStart());
       if (send) CK_NCCL(c, ncclSend(c->x, (size_t)cur.n() * d, ncclFloat32, p + 1, c->comm, c->st));
       if (recv) CK_NCCL(c, ncclRecv(c->hin, (size_t)prev.n() * d, ncclFloat32, p - 1, c->comm, c->st));
+      if (out_rows)
+        CK_NCCL(c, ncclBroadcast(c->res, c->res, (size_t)outseg.n() * 2, ncclInt32, P - 1, c->comm, c->st));
       CK_NCCL(c, ncclGroupEnd());
     }
   }
   for (int q = 0; q < P; q++)
     if (c->slot[q].valid()) c->n_cached[q] = std::max(c->n_cached[q], c->slot[q].e);
-  const Seg outseg = c->slot[P - 1];
   if (out) {
     out->seg_id = outseg.valid() ? outseg.id : -1;
     out->s_begin = outseg.b;
     out->n_rows = outseg.valid() ? outseg.n() : 0;
   }
-  if (outseg.valid() && outseg.n() > 0) {
+  if (out_rows) {
     const int n = outseg.n();
-    if (P > 1)
-      CK_NCCL(c, ncclBroadcast(c->res, c->res, (size_t)n * 2, ncclInt32, P - 1, c->comm, c->st));
     commit_rows_kernel<<<1, FS_MAX_SEG, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->out_node);
     CK_LAUNCH(c);
     CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * n, cudaMemcpyDeviceToHost, c->st));
