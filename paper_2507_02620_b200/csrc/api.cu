@@ -100,7 +100,6 @@ struct fs_ctx {
   int* gcnt = nullptr;
   Top2* head_part = nullptr;
   RowResult* res = nullptr;
-  int32_t* out_node = nullptr;
   float *aws_o = nullptr, *aws_ml = nullptr;
   int* att_cnt = nullptr;
   unsigned long long* att_dbg = nullptr;  // FS_ATT_DEBUG diagnostics only
@@ -363,7 +362,6 @@ size_t carve(fs_ctx* c, char* base) {
   c->ssq = cv.take<float>((size_t)((d + 127) / 128) * 4 * np);
   c->head_part = cv.take<Top2>((size_t)((V + 127) / 128) * np);
   c->res = cv.take<RowResult>(FS_MAX_SEG);
-  c->out_node = cv.take<int32_t>(FS_MAX_SEG);
   c->att_chunk_cap = (f.max_ctx + ATT_KC - 1) / ATT_KC;
   const int G = H / Hkv;
   c->aws_o = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * ATT_HD) : nullptr;
@@ -1329,28 +1327,24 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
   }
   if (out_rows) {
     const int n = outseg.n();
-    commit_rows_kernel<<<1, FS_MAX_SEG, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->out_node);
-    CK_LAUNCH(c);
-    CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * n, cudaMemcpyDeviceToHost, c->st));
-    CK_CUDA(c, cudaMemcpyAsync(c->h_node, c->out_node, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
-    // the accept walk (fs_accept) over the updated tree, under the same sync
+    // commit the rows, then the accept walk over the updated tree and the
+    // prune plan of its decision (fs_accept / fs_prune_and_compact consume them
+    // without another device round trip): one kernel, one read-back
     c->acc_ready = false;
     c->plan_ready = false;
-    if (c->live && c->n_live > 0) {
-      accept_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live, 1e-2f);
-      CK_LAUNCH(c);
-      prune_plan_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live);
-      CK_LAUNCH(c);
-      CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
-      c->acc_ready = true;
-      c->plan_ready = true;
-    }
+    const bool acc = c->live && c->n_live > 0;
+    post_tick_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->d_rec, c->n_live,
+                                                    acc ? 1 : 0, 1e-2f);
+    CK_LAUNCH(c);
+    CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+    c->acc_ready = acc;
+    c->plan_ready = acc;
     if ((rc = sync(c))) return rc;
     if (out)
       for (int m = 0; m < n; m++) {
-        out->node[m] = c->h_node[m];
-        out->am[m] = c->h_res[m].am;
-        out->margin[m] = c->h_res[m].margin;
+        out->node[m] = c->h_rec->tick_node[m];
+        out->am[m] = c->h_rec->tick_res[m].am;
+        out->margin[m] = c->h_rec->tick_res[m].margin;
       }
   } else {
     if ((rc = sync(c))) return rc;

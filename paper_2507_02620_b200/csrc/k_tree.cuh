@@ -192,8 +192,7 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
 
 // ---------------------------------------------------------------- accept
 // Greedy acceptance + continuous condition (Eq. 2; R1, R3, R23).
-__global__ void __launch_bounds__(TREE_THREADS) accept_kernel(TreeDev t, TreeRecord* rec,
-                                                              int32_t n_live, float flag_margin) {
+FS_DEV void accept_walk(TreeDev t, TreeRecord* rec, int32_t n_live, float flag_margin) {
   __shared__ int s_child;
   __shared__ int s_v;
   __shared__ int s_nacc;
@@ -376,8 +375,7 @@ __global__ void __launch_bounds__(TREE_THREADS) prune_kernel(TreeDev t, const De
 // The rank map and |I_pr| prune_kernel derives from the decision accept_kernel
 // just recorded (same membership rule: I_acc, plus n_new and its descendants
 // by the ancestor bitset when the round continues), without touching the tree.
-__global__ void __launch_bounds__(TREE_THREADS) prune_plan_kernel(TreeDev t, TreeRecord* rec,
-                                                                  int32_t n_live) {
+FS_DEV void prune_plan(TreeDev t, TreeRecord* rec, int32_t n_live) {
   __shared__ unsigned char s_is_acc[MAXLIVE];
   __shared__ int s_warp[TREE_THREADS / 32 + 1];
   const int i = threadIdx.x;
@@ -399,6 +397,39 @@ __global__ void __launch_bounds__(TREE_THREADS) prune_plan_kernel(TreeDev t, Tre
   block_excl_count(in_pr, s_warp, &n_pr);
   if (i < MAXLIVE) rec->spec_rank[i] = (i < n_live && ret) ? r : -1;
   if (i == 0) rec->spec_n_pr = ok ? n_pr : -1;
+}
+
+__global__ void __launch_bounds__(TREE_THREADS) accept_kernel(TreeDev t, TreeRecord* rec, int32_t n_live,
+                                                              float flag_margin) {
+  accept_walk(t, rec, n_live, flag_margin);
+}
+
+__global__ void __launch_bounds__(TREE_THREADS) prune_plan_kernel(TreeDev t, TreeRecord* rec, int32_t n_live) {
+  prune_plan(t, rec, n_live);
+}
+
+// The verify step's tail in one launch: commit the output segment's row
+// results into the tree (am, margin, verified) and copy them with the node
+// ids into the record; then (do_accept) the accept walk and the prune plan
+// of its decision.  The record is read back with one copy.
+__global__ void __launch_bounds__(TREE_THREADS) post_tick_kernel(TreeDev t, const RowResult* res, int32_t s_begin,
+                                                                 int32_t n_rows, TreeRecord* rec, int32_t n_live,
+                                                                 int32_t do_accept, float flag_margin) {
+  const int m = threadIdx.x;
+  if (m < n_rows) {
+    const int s = s_begin + m;
+    const RowResult r = res[m];
+    t.am[s] = r.am;
+    t.margin[s] = r.margin;
+    t.verified[s] = 1;
+    rec->tick_res[m] = r;
+    rec->tick_node[m] = t.node[s];
+  }
+  if (!do_accept) return;
+  __syncthreads();   // the committed rows are visible to the whole block
+  accept_walk(t, rec, n_live, flag_margin);
+  __syncthreads();
+  prune_plan(t, rec, n_live);
 }
 
 // ---------------------------------------------------------------- KV compaction
@@ -464,20 +495,6 @@ __global__ void tick_setup_kernel(TreeDev t, TickRows* rows, int32_t s_begin, in
     rows->l_glo = l_glo;
     rows->n_keys = l_glo + s_begin + n_rows;
     rows->s_begin = s_begin;
-  }
-}
-
-// Store the verified rows' argmax/margin in the tree replica, mark verified,
-// and gather node ids for the host record.
-__global__ void commit_rows_kernel(TreeDev t, const RowResult* res, int32_t s_begin,
-                                   int32_t n_rows, int32_t* out_node) {
-  const int m = threadIdx.x;
-  if (m < n_rows) {
-    const int s = s_begin + m;
-    t.am[s] = res[m].am;
-    t.margin[s] = res[m].margin;
-    t.verified[s] = 1;
-    out_node[m] = t.node[s];
   }
 }
 

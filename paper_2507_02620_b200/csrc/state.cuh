@@ -63,6 +63,9 @@ struct TreeRecord {
   // passes the decision fs_accept returned (prune_plan_kernel)
   int32_t spec_n_pr;
   int32_t spec_rank[MAXLIVE];
+  // verify step: the output segment's row results and node ids (one D2H with the record)
+  RowResult tick_res[FS_MAX_SEG];
+  int32_t tick_node[FS_MAX_SEG];
 };
 
 // Input of the submit kernel (copied host -> device)
