@@ -465,7 +465,10 @@ __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks, int n_parts_f
 // r, r+nsplit, ... of all splits through distributed shared memory (split
 // order: deterministic) and writes the bf16 hi/lo attention output pair.
 constexpr int ATT_SUB = 64;   // keys per sub-chunk
-constexpr int ATT_NBUF = 3;   // sub-chunk ring depth
+#ifndef FS_ATT_NBUF
+#define FS_ATT_NBUF 3
+#endif
+constexpr int ATT_NBUF = FS_ATT_NBUF;   // sub-chunk ring depth
 constexpr int ATT_MAXQR = 32;
 constexpr int ATT_SO_LD = ATT_HD + 8;   // padded row of the key-warp state scratch (float2
                                         // stores of a half-warp: 4 rows x 8 banks, conflict-free)
