@@ -17,14 +17,17 @@ def _hilo(x):
     return (hi + lo).double().numpy()
 
 
-@pytest.mark.parametrize("name,which", [("small", 1), ("7b_l2", 0), ("7b_l2", 1), ("7b_l2", 3)])
-def test_gemm_matches_fp64(name, which):
+@pytest.mark.parametrize("name,which,rows,max_seg", [("small", 1, 13, 16), ("7b_l2", 0, 13, 16),
+                                                     ("7b_l2", 1, 13, 16), ("7b_l2", 3, 13, 16),
+                                                     ("7b_l2", 0, 61, 64), ("7b_l2", 1, 61, 64),
+                                                     ("7b_l2", 3, 29, 32)])
+def test_gemm_matches_fp64(name, which, rows, max_seg):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from paper_2507_02620_b200 import flowspec as F
     shape = SHAPES[name]
-    gp = F.Pipeline(shape, max_ctx=1024, max_seg=16)
+    gp = F.Pipeline(shape, max_ctx=1024, max_seg=max_seg)
     gp.fs_load_random_weights(11)
     gp.fs_set_prefix([1, 2, 3])
     model = fso.Model(shape, 11)
@@ -35,7 +38,7 @@ def test_gemm_matches_fp64(name, which):
     else:
         W = model.tensor(fso.DOWN)
     rng = np.random.default_rng(0)
-    X = rng.standard_normal((13, W.shape[1])).astype(np.float32)
+    X = rng.standard_normal((rows, W.shape[1])).astype(np.float32)
     Y = gp.debug_gemm(0, which, X, W.shape[0])
     ref = _hilo(X) @ W.astype(np.float64).T
     err = np.abs(Y - ref)

@@ -191,3 +191,16 @@ def test_error_codes_leave_state_unchanged():
     assert state() == s1
     o = gp.fs_verify_step()
     assert o["n_rows"] == 3
+
+
+@pytest.mark.parametrize("name", ["small", "smallq"])
+def test_bf16_wide_segments_lockstep(name):
+    """max_seg = FS_MAX_SEG (64): the N = 64 GEMM configuration (one CTA per SM,
+    its own split planning), 64-row prefill chunks, and a 60-node tree verified
+    as one segment (ragged against the 64-row tile) next to 64-row segments."""
+    F, shape, gp, op, xo, xg = _pair(name, max_ctx=1024, max_seg=64, prefix_len=150)
+    st = run_lockstep(gp, op, planted_trees(shape, 60, 5, (0, 2, 5, 17, 21), SEED), n_rounds=2,
+                      l_max=64, tol=2e-2)
+    assert st.max_abs <= 2e-2
+    print(f"{name} wide: max|dlogit| {st.max_abs:.3e} rows {st.rows} flagged {st.flagged} "
+          f"overrides {st.overrides}")
