@@ -204,3 +204,13 @@ def test_bf16_wide_segments_lockstep(name):
     assert st.max_abs <= 2e-2
     print(f"{name} wide: max|dlogit| {st.max_abs:.3e} rows {st.rows} flagged {st.flagged} "
           f"overrides {st.overrides}")
+
+
+def test_tiny_capacity_tree_max_live():
+    """A 500-node tree against max_live = 512: submit (score order, 16-word
+    ancestor bitsets), segment scheduling and prune at capacity, in lockstep."""
+    F, shape, gp, op, xo, xg = _pair("tiny", max_ctx=1024, max_live=512)
+    st = run_lockstep(gp, op, planted_trees(shape, 500, 9, (0, 3, 40, 170, 333, 401), SEED), n_rounds=1,
+                      l_max=16, tol=1e-4)
+    assert st.max_abs <= 1e-4
+    print(f"tiny capacity: max|dlogit| {st.max_abs:.3e} rows {st.rows} decisions {st.decisions}")
