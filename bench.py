@@ -109,6 +109,20 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ our arm
+PRUNES = [0]   # fs_prune_and_compact calls (host -> device decision copies)
+
+# bytes the library copies per call (include/flowspec.h capacities: FS_MAX_LIVE
+# 512, FS_MAX_SEG 64): SubmitIn (5 ints + parent / token / own [512]) host ->
+# device per submit; the submit record prefix (11 ints + order [512]) back;
+# the verify step's record (11 ints, 5 x [512] arrays, prune plan 1 + [512],
+# 64 row results of 8 B and 64 node ids) back per tick; DecisionIn (4 ints +
+# acc ids [512]) host -> device per prune
+H2D_SUBMIT = 4 * (5 + 3 * 512)
+D2H_SUBMIT = 4 * (11 + 512)
+D2H_TICK = 4 * (11 + 5 * 512 + 1 + 512) + 64 * 8 + 64 * 4
+H2D_PRUNE = 4 * (4 + 512)
+
+
 def run_round(gp, tree, l_max, tokens_out=None):
     """One SD round: submit, ticks, accept, prune until the round exits."""
     from paper_2507_02620_b200 import flowspec as F
@@ -125,6 +139,7 @@ def run_round(gp, tree, l_max, tokens_out=None):
         if tokens_out is not None:
             tokens_out += list(d.acc_tokens[:d.n_acc])
         gp.fs_prune_and_compact(d)
+        PRUNES[0] += 1
         if not d.cont:
             return committed, ticks
 
@@ -229,10 +244,12 @@ def ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     tokens = ticks = 0
+    prunes0 = PRUNES[0]
     for r in range(W, W + K):
         c, t = round_r(r)
         tokens += c
         ticks += t
+    prunes = PRUNES[0] - prunes0
     e1.record(st)
     torch.cuda.synchronize()
     if P > 1:
@@ -305,7 +322,6 @@ def ours(args):
 
     if rank != 0:
         return
-    n_tree_bytes = n_nodes * 12
     rec = {
         "metric": "accepted tokens/s (pipelined tree verify)",
         "value": round(value, 3),
@@ -336,8 +352,10 @@ def ours(args):
         },
         "clocks": clk,
         "e2e": {"value": round(e2e, 3), "unit": "tok/s",
-                "h2d_bytes_per_step": n_tree_bytes + 8 * 64,
-                "d2h_bytes_per_step": 4700 * 4},
+                "h2d_bytes_per_step": round(H2D_SUBMIT + H2D_PRUNE * prunes / K),
+                "d2h_bytes_per_step": round(D2H_SUBMIT + D2H_TICK * ticks / K),
+                "bytes_note": "the library's whole-struct copies per submit / tick / prune (bench.py "
+                              "H2D_SUBMIT, D2H_TICK, ...), not just the live entries"},
         "gpu_launches": int(launches),
     }
     if prof:
