@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   uint64_t* s_full = empty + C::NST;     // [MT2]
   uint64_t* p_full = s_full + 2;         // [MT2]
   uint64_t* pv_done = p_full + 2;        // [MT2]: P V of the step complete (S/P columns free)
-  uint64_t* o_full = pv_done + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
+  uint64_t* o_full = pv_done + 2;        // [MT2]: the M-tile's last P V complete
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
   int* sCtxMin = reinterpret_cast<int*>(tmem_holder + 1);
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256);
 
@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       mbar_init(&p_full[mi], 128);
       mbar_init(&pv_done[mi], 1);
     }
-    mbar_init(o_full, 1);
+    mbar_init(&o_full[0], 1);
+    mbar_init(&o_full[1], 1);
     fence_barrier_init();
   }
   const int n_rows = rows->n_rows;
@@ -268,11 +269,11 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       for (int j = 0; j < T; j++) {
         for (int mi = 0; mi < MT2; mi++) {
           issue_pv(j, mi);
+          if (j + 1 == T) umma_commit(&o_full[mi]);   // M-tile mi's O is final: its epilogue may start
           if (j + 1 < T) issue_qk(j + 1, mi);
         }
         umma_commit(&empty[stage_of(j)]);   // stage j's K / V reads are all issued
       }
-      umma_commit(o_full);
     }
     __syncwarp();
   } else {
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     // ---------------- unnormalised O row and (M, l) of this split
     TCA_PROBE(7);
-    mbar_wait(o_full, 0);
+    mbar_wait(&o_full[mi], 0);
     tc_fence_after();
     TCA_PROBE(8);
     // every MMA has completed: the Q / K / V buffers stage the warp's 32 rows
