@@ -6,10 +6,12 @@
  * contract stores them:
  *   residual x ............ fp32
  *   q, k, v (after bias+RoPE) bf16 (K/V cache storage)
- *   RMSNorm output, attention output, silu(g)*u (the GEMM inputs):
- *                           fp32 carried as bf16 hi + bf16 lo; an RMSNorm feeding
- *                           a linear layer is applied as inv * (W (x*g))
+ *   RMSNorm output, attention output, silu(g)*u (the GEMM inputs): fp32
  *   logits ................ fp32
+ * i.e. the bf16 branch differs from the fp32 one only in the weights and in
+ * the q/k/v storage; every other step is the plain definition (RMSNorm
+ * y = x*inv*g, then the linear layer), pinned against HF transformers in
+ * tests/test_oracle_decoder.py (fp32, and bf16 with the same storage points).
  * (fp32 config: fp32 everywhere)
  * Compile with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
  *
@@ -334,24 +336,19 @@ static float store_act(const fso_cfg* c, double v) {
   return c->bf16 ? fso_round_bf16(f) : f;
 }
 
-/* GEMM-input activations (RMSNorm outputs, attention output, silu*up): fp32,
- * carried under the bf16 contract as a pair of bf16 values hi + lo with
- * hi = bf16(f), lo = bf16(f - hi)  (R18) */
-static double store_act2(const fso_cfg* c, double v) {
-  float f = (float)v;
-  if (!c->bf16) return f;
-  float hi = fso_round_bf16(f);
-  float lo = fso_round_bf16(f - hi);
-  return (double)hi + (double)lo;
-}
+/* GEMM-input activations (RMSNorm outputs, attention output, silu*up) are
+ * stored as fp32 under both contracts (R18) */
+static double store_f32(double v) { return (double)(float)v; }
 
-/* RMSNorm (LLaMA): RMSNorm(x) = x * inv * g with inv = 1/sqrt(mean(x^2) + eps).
- * fp32 configs: y = fp32(x * inv * g), scale = 1.
- * bf16 configs (R18): the norm feeds a linear layer, and
- * W (x * inv * g) = inv * (W (x * g)); the GEMM input is y = hi/lo pair of
- * fp32(x * g) and the linear output is multiplied by scale = inv afterwards. */
+/* Mutation switch for the pin tests only (tests/test_oracle_decoder.py):
+ * each value removes one term so the test can show its pin notices. 0 = off. */
+static int32_t g_mutant = 0;
+void fso_set_mutant(int32_t which) { g_mutant = which; }
+
+/* RMSNorm (LLaMA, PAPER.md:721 decoder layer; HF LlamaRMSNorm):
+ *   y = x * inv * g,  inv = 1/sqrt(mean(x^2) + eps), stored as fp32. */
 static void rmsnorm(fso_model* m, int32_t layer, int32_t which, int32_t n_rows,
-                    const float* x, double* y, double* scale) {
+                    const float* x, double* y) {
   const fso_cfg* c = &m->c;
   int32_t d = c->d_model;
   float* g = (float*)malloc((size_t)d * 4);
@@ -360,22 +357,12 @@ static void rmsnorm(fso_model* m, int32_t layer, int32_t which, int32_t n_rows,
     double ss = 0.0;
     for (int32_t k = 0; k < d; k++) ss += (double)x[(int64_t)r * d + k] * (double)x[(int64_t)r * d + k];
     double inv = 1.0 / sqrt(ss / d + c->rms_eps);
-    if (c->bf16) {
-      scale[r] = inv;
-      for (int32_t k = 0; k < d; k++)
-        y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * (double)g[k]);
-    } else {
-      scale[r] = 1.0;
-      for (int32_t k = 0; k < d; k++)
-        y[(int64_t)r * d + k] = store_act2(c, (double)x[(int64_t)r * d + k] * inv * (double)g[k]);
-    }
+    if (g_mutant == 1 && which == FSO_FINAL_NORM) inv = 1.0;   /* mutant: no inv on the head */
+    if (g_mutant == 2 && which == FSO_ATTN_NORM) inv = 1.0;    /* mutant: no inv before QKV */
+    for (int32_t k = 0; k < d; k++)
+      y[(int64_t)r * d + k] = store_f32((double)x[(int64_t)r * d + k] * inv * (double)g[k]);
   }
   free(g);
-}
-
-static void scale_rows(double* out, int32_t n_rows, int64_t n_cols, const double* scale) {
-  for (int32_t r = 0; r < n_rows; r++)
-    for (int64_t j = 0; j < n_cols; j++) out[(int64_t)r * n_cols + j] *= scale[r];
 }
 
 /* out[m][r] = sum_k W[r][k] * in[m][k]  (fp64 accumulation, k ascending) */
@@ -459,17 +446,13 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
   double* u = (double*)malloc((size_t)n_rows * c->ffn * 8);
   double* o = (double*)malloc((size_t)n_rows * wmax * 8);
   float* bias = (float*)malloc((size_t)nq * 4);
-  double* rs = (double*)malloc((size_t)n_rows * 8);
 
   for (int32_t l = layer_begin; l < layer_end; l++) {
     /* --- self-attention block --- */
-    rmsnorm(m, l, FSO_ATTN_NORM, n_rows, x, y, rs);
+    rmsnorm(m, l, FSO_ATTN_NORM, n_rows, x, y);
     linear(m, l, FSO_Q, n_rows, y, q);
     linear(m, l, FSO_K, n_rows, y, kk);
     linear(m, l, FSO_V, n_rows, y, vv);
-    scale_rows(q, n_rows, nq, rs);
-    scale_rows(kk, n_rows, nkv, rs);
-    scale_rows(vv, n_rows, nkv, rs);
     if (c->qkv_bias) {
       get_row(m, l, FSO_BQ, 0, bias);
       for (int32_t r = 0; r < n_rows; r++)
@@ -524,21 +507,19 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
           double p = s[j] / den;
           for (int32_t t = 0; t < hd; t++) oh[t] += p * kv_load(kv, vb + t);
         }
-        for (int32_t t = 0; t < hd; t++) oh[t] = store_act2(c, oh[t]);
+        for (int32_t t = 0; t < hd; t++) oh[t] = store_f32(oh[t]);
         free(s);
       }
     linear(m, l, FSO_O, n_rows, att, o);
     for (int64_t i = 0; i < (int64_t)n_rows * d; i++) x[i] = (float)((double)x[i] + o[i]);
 
     /* --- SwiGLU FFN block --- */
-    rmsnorm(m, l, FSO_MLP_NORM, n_rows, x, y, rs);
+    rmsnorm(m, l, FSO_MLP_NORM, n_rows, x, y);
     linear(m, l, FSO_GATE, n_rows, y, g);
     linear(m, l, FSO_UP, n_rows, y, u);
-    scale_rows(g, n_rows, c->ffn, rs);
-    scale_rows(u, n_rows, c->ffn, rs);
     for (int64_t i = 0; i < (int64_t)n_rows * c->ffn; i++) {
       double gv = g[i];
-      g[i] = store_act2(c, gv / (1.0 + exp(-gv)) * u[i]);
+      g[i] = store_f32(gv / (1.0 + exp(-gv)) * u[i]);   /* SiLU(g) * u */
     }
     linear(m, l, FSO_DOWN, n_rows, g, o);
     for (int64_t i = 0; i < (int64_t)n_rows * d; i++) x[i] = (float)((double)x[i] + o[i]);
@@ -546,17 +527,15 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin, int32_t layer
 
   if (h_out) memcpy(h_out, x, (size_t)n_rows * d * 4);
   if (layer_end == c->n_layers && logits) {
-    rmsnorm(m, 0, FSO_FINAL_NORM, n_rows, x, y, rs);
+    rmsnorm(m, 0, FSO_FINAL_NORM, n_rows, x, y);
     int64_t V = c->vocab;
     double* lg = (double*)malloc((size_t)n_rows * V * 8);
     linear(m, 0, FSO_HEAD, n_rows, y, lg);
-    scale_rows(lg, n_rows, V, rs);
     for (int64_t i = 0; i < (int64_t)n_rows * V; i++) logits[i] = (float)lg[i];
     free(lg);
   }
   free(x); free(y); free(q); free(kk); free(vv); free(att); free(g); free(u); free(o);
   free(bias);
-  free(rs);
   return 0;
 }
 

@@ -89,6 +89,11 @@ int32_t fso_forward(fso_model* m, fso_kv* kv, int32_t layer_begin,
                     const int32_t* vis_off, const int32_t* vis_slot,
                     const float* h_in, float* h_out, float* logits);
 
+/* Pin tests only: 1 = drop inv of the final RMSNorm (head), 2 = drop inv of
+ * the attention RMSNorm (QKV); 0 = the oracle as specified.  Lets a test show
+ * that its pin fails on a plausible mistake. */
+void fso_set_mutant(int32_t which);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,7 @@ def lib():
         L.fso_kv_synth.argtypes = [P, C.c_int32, C.c_uint64]
         L.fso_forward.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, i32p, i32p, i32p,
                                   i32p, i32p, f32p, f32p, f32p]
+        L.fso_set_mutant.argtypes = [C.c_int32]
         _lib = L
     return _lib
 

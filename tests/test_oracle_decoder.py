@@ -70,6 +70,17 @@ def test_generator_grid_and_moments():
 
 
 # ------------------------------------------------------------------ HF pin
+def _bf16_storage_attention(module, query, key, value, attention_mask, scaling,
+                            dropout=0.0, **kw):
+    """HF eager attention with q, K and V stored as bf16 after bias + RoPE — the
+    storage points of the bf16 precision contract (R18: the KV cache
+    and q are bf16); everything else stays HF's own fp32 arithmetic."""
+    from transformers.models.llama.modeling_llama import eager_attention_forward
+    r = lambda t: t.to(torch.bfloat16).to(t.dtype)
+    return eager_attention_forward(module, r(query), r(key), r(value), attention_mask,
+                                   scaling, dropout, **kw)
+
+
 def _hf_model(shape, model):
     from transformers import LlamaConfig, LlamaForCausalLM, Qwen2Config, Qwen2ForCausalLM
     kw = dict(vocab_size=shape.vocab, hidden_size=shape.d_model, intermediate_size=shape.ffn,
@@ -82,7 +93,24 @@ def _hf_model(shape, model):
         hf = Qwen2ForCausalLM(Qwen2Config(**kw))
     else:
         hf = LlamaForCausalLM(LlamaConfig(attention_bias=False, **kw))
-    hf.config._attn_implementation = "eager"
+    if shape.bf16:
+        from transformers import AttentionInterface
+        AttentionInterface.register("bf16_storage", _bf16_storage_attention)
+        hf.config._attn_implementation = "bf16_storage"
+        # the contract's RoPE tables: angle in fp64, cos/sin rounded to fp32
+        # (DESIGN.md "RoPE tables"); HF's own fp32 angle differs by ~1e-6 at
+        # position 40 and would only add bf16 rounding flips of q/K
+        hd, theta = shape.head_dim, shape.rope_theta
+
+        def rope64(x, position_ids):
+            inv = theta ** (-torch.arange(0, hd, 2, dtype=torch.float64) / hd)
+            ang = position_ids[0].to(torch.float64)[:, None] * inv[None, :]
+            emb = torch.cat((ang, ang), dim=-1)[None]
+            dt = x.dtype
+            return emb.cos().float().to(dt), emb.sin().float().to(dt)
+        hf.model.rotary_emb.forward = rope64
+    else:
+        hf.config._attn_implementation = "eager"
     sd = {"model.embed_tokens.weight": model.tensor(fso.EMBED),
           "lm_head.weight": model.tensor(fso.HEAD),
           "model.norm.weight": model.tensor(fso.FINAL_NORM)}
@@ -105,6 +133,77 @@ def _hf_model(shape, model):
     missing, unexpected = hf.load_state_dict(sd, strict=False)
     assert not unexpected and all("rotary" in m for m in missing), (missing, unexpected)
     return hf.eval()
+
+
+def _hf_tree_logits(shape, name, mutant=0, hf64=False):
+    """Oracle tree verification and HF over prefix ++ S with tree position ids
+    and a custom 4D additive mask; returns (oracle prefix logits, oracle tree
+    logits, HF logits, n_pre, x_new).  hf64: HF in fp64 arithmetic."""
+    n_pre = 20
+    fso.lib().fso_set_mutant(mutant)
+    try:
+        op = OraclePipeline(shape, SEED, n_stages=1)
+        prefix = gen.prefix_tokens(11, n_pre, shape.vocab)
+        x_new = op.set_prefix(prefix)
+        t = gen.random_tree(5, 24, 5, shape.vocab, x_new)
+        sub = op.submit(True, t["parent"], t["token"], t["own"], l_max=24)
+        out = op.verify_step()
+    finally:
+        fso.lib().fso_set_mutant(0)
+    snap = op.snapshot()
+    m = len(sub["order"])
+    hf = _hf_model(shape, op.model)
+    dt = torch.float64 if hf64 else torch.float32
+    hf = hf.to(dt)
+    ids = list(prefix) + snap["token"]
+    pos = list(range(n_pre)) + snap["pos"]
+    L = n_pre + m
+    mask = torch.full((1, 1, L, L), torch.finfo(dt).min, dtype=dt)
+    for i in range(n_pre):
+        mask[0, 0, i, :i + 1] = 0
+    for k in range(m):
+        mask[0, 0, n_pre + k, :n_pre] = 0
+        for a in snap["anc"][k]:
+            mask[0, 0, n_pre + k, n_pre + a] = 0
+    with torch.no_grad():
+        lg = hf(input_ids=torch.tensor([ids]), position_ids=torch.tensor([pos]),
+                attention_mask=mask).logits[0].double().numpy()
+    return op.prefix_logits, out["logits"], lg, n_pre, x_new
+
+
+# bf16 bound.  The oracle (fp64 arithmetic, fp32 activations) and HF run in
+# fp64 round q/K/V to bf16 at the same storage points, so they differ by the fp32
+# rounding of the oracle's activations (relative 2^-24) and by the bf16 rounding
+# flips that difference causes (a stored element whose two values straddle a
+# bf16 boundary moves by one bf16 ulp, 2^-8 relative).  HF in fp32 arithmetic is
+# a second correct implementation of the same contract with ~2^7x larger
+# arithmetic error, hence more flips: |HF32 - HF64| is the contract's inherent
+# spread, and the oracle must sit well inside it.  A hard cap keeps the pin
+# meaningful on its own.
+def _bf16_pin_errors(name, mutant=0):
+    shape = SHAPES[name]
+    pre, tree, lg64, n, _ = _hf_tree_logits(shape, name, mutant=mutant, hf64=True)
+    _, _, lg32, _, _ = _hf_tree_logits(shape, name, hf64=False)
+    o = np.concatenate([pre[None].astype(np.float64), tree.astype(np.float64)])
+    return float(np.max(np.abs(o - lg64[n - 1:]))), float(np.max(np.abs(lg32[n - 1:] - lg64[n - 1:])))
+
+
+@pytest.mark.parametrize("name", ["small", "smallq"])
+def test_bf16_tree_verification_matches_hf(name):
+    """bf16 branch of the oracle against HF on the same bf16-rounded weights,
+    with q/K/V stored as bf16 and the contract's RoPE tables (R18):
+    pins the plain RMSNorm -> linear order, the bias, RoPE and the storage
+    points of the bf16 branch."""
+    err, spread = _bf16_pin_errors(name)
+    assert err <= 0.5 * spread and err <= 1e-3, (err, spread)
+
+
+@pytest.mark.parametrize("mutant", [1, 2])
+def test_bf16_hf_pin_catches_dropped_norm_scale(mutant):
+    """A mistake in the bf16 branch (RMSNorm scale dropped before the head or
+    before QKV) must fail the pin above by orders of magnitude."""
+    err, _ = _bf16_pin_errors("small", mutant)
+    assert err > 1.0, err      # the pin's cap is 1e-3
 
 
 @pytest.mark.parametrize("name", ["tiny", "tinyq"])
