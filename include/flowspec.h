@@ -45,6 +45,21 @@ extern "C" {
 #define FS_MAX_SEG 64      /* hard cap on rows per segment */
 #define FS_MAX_STAGES 8
 
+/* Single-process transport between the stage contexts of one pipeline (one
+ * context per stage, each driven by its own host thread, SPMD as with NCCL):
+ * the collective calls (fs_set_prefix, fs_verify_step) exchange the hidden
+ * rows p -> p+1 ("the intermediate result ... sent to V2") and the last
+ * stage's row results as device-to-device copies ordered by CUDA events — the
+ * same schedule and bytes as the NCCL path, so a P-stage pipeline runs (and is
+ * tested) on one GPU.  Every stage's collective call must be in flight
+ * concurrently (one thread per context); a peer that does not arrive within
+ * 120 s fails the call with FS_ENCCL and poisons the context. */
+typedef struct fs_local_group fs_local_group;
+/* Create a group for n_stages contexts.  FS_EINVAL for n_stages outside
+ * 2..FS_MAX_STAGES.  The caller owns it; destroy after every member context. */
+int fs_local_group_create(int32_t n_stages, fs_local_group** out);
+void fs_local_group_destroy(fs_local_group* g);
+
 typedef struct fs_config {
   /* model shape (LLaMA2 / Qwen2 decoder, App. B.1; R19) */
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn, vocab;
@@ -69,6 +84,11 @@ typedef struct fs_config {
   size_t arena_bytes;
   void* stream;             /* cudaStream_t the library issues all work on */
   const uint8_t* nccl_id;   /* 128-byte ncclUniqueId from rank 0 (n_stages > 1) */
+  fs_local_group* local_group; /* n_stages > 1 without NCCL: all stages are
+                               contexts of THIS process (same or peer-accessible
+                               devices), the stage transport (a10) is a device
+                               copy through the group.  Exactly one of nccl_id /
+                               local_group must be set when n_stages > 1. */
 } fs_config;
 
 typedef struct fs_ctx fs_ctx;
@@ -86,7 +106,8 @@ int fs_layers_per_stage(const fs_config* cfg, int32_t* out);
 int fs_nccl_unique_id(uint8_t* out);
 
 /* Create a context.  Validates cfg (FS_EINVAL), checks the arena
- * (FS_ENOMEM), joins the NCCL communicator when n_stages > 1. */
+ * (FS_ENOMEM), joins the NCCL communicator (or registers as stage `rank` of
+ * cfg->local_group, FS_EINVAL if that rank is taken) when n_stages > 1. */
 int fs_init(const fs_config* cfg, fs_ctx** out);
 
 /* Fill this rank's weights (its layer block; embedding on stage 0; final norm

@@ -10,7 +10,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -71,6 +75,24 @@ struct LayerW {
 
 }  // namespace
 
+// Single-process stage transport (include/flowspec.h fs_local_group): a
+// channel per (src, dst) pair carries one posted buffer at a time; the
+// receiver pulls it with a device copy on its own stream after the sender's
+// ready event and acknowledges with its own done event, on which the sender's
+// stream then waits (the sender may not overwrite the buffer before the copy).
+struct fs_local_group {
+  int P = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Chan {
+    uint64_t posted = 0, taken = 0;
+    const void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t ready = nullptr, done = nullptr;
+  } ch[FS_MAX_STAGES][FS_MAX_STAGES];
+  fs_ctx* member[FS_MAX_STAGES] = {};
+};
+
 struct fs_ctx {
   fs_config cfg;
   int lps[FS_MAX_STAGES];
@@ -81,6 +103,9 @@ struct fs_ctx {
   int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
+  fs_local_group* lg = nullptr;           // single-process stage transport (else NCCL)
+  cudaEvent_t ev_ready = nullptr;         // local transport: this rank's outgoing data ready
+  cudaEvent_t ev_done[FS_MAX_STAGES] = {}; // local transport: copy from rank q finished
   // arena
   char* base = nullptr;
   size_t off = 0, cap = 0;
@@ -492,10 +517,23 @@ void prof_end(fs_ctx* c, int idx) {
 }
 
 // ---------------------------------------------------------------- launches
+// kernel attributes are per device: set them once on every device a context uses
+// (double-checked under a lock: contexts of a local group launch from several threads)
+template <typename F>
+void once_per_device(std::atomic<uint64_t>& done, const fs_ctx* c, F set) {
+  static std::mutex mu;
+  const uint64_t bit = 1ull << (c->cfg.device & 63);
+  if (done.load() & bit) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.load() & bit) return;
+  set();
+  done.fetch_or(bit);
+}
+
 template <int NT>
 int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, c, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          GemmCfg<NT>::SMEM);
     cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -504,8 +542,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
     cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          GemmCfg<NT>::SMEM);
     cudaFuncSetAttribute(gemm_cluster_kernel<NT, NT / 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
-  }
+  });
   if (g.split > 0) {
     GemmShape sh = g.sh;
     sh.dbg = nullptr;
@@ -647,12 +684,11 @@ int launch_attention(fs_ctx* c, int l) {
       ma.out = (bf16*)c->att;
       const size_t smem = (size_t)QR * ATT_LD * 2 + (size_t)ATT_NBUF * 2 * ATT_SUB * ATT_LD * 2 +
                           (size_t)np * c->ancw * 4 + 16;
-      static bool mattr = false;
-      if (!mattr) {
+      static std::atomic<uint64_t> mattr{0};
+      once_per_device(mattr, c, [] {
         cudaFuncSetAttribute(attn_mha_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         cudaFuncSetAttribute(attn_mha_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        mattr = true;
-      }
+      });
       // cluster of key splits per kv head (sizes read on device): the largest
       // split count <= 8 whose Hkv clusters are all co-resident (one wave;
       // clusters must fit inside a GPC, so this is below 2 * SMs / Hkv)
@@ -751,11 +787,10 @@ int launch_attention(fs_ctx* c, int l) {
     }
     const int n_chunks = (n_keys + ATT_KC - 1) / ATT_KC;
     const size_t smem = (size_t)QR * ATT_LD * 2 + 2 * ATT_KC * ATT_LD * 2 + (size_t)np * c->ancw * 4;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, c, [] {
       cudaFuncSetAttribute(attn_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    });
     const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
                                          (double)n_chunks * KS * Hkv * QR * (hd + 2) * 4);
     attn_mma_kernel<<<dim3(c->att_chunk_cap, Hkv), 128, smem, c->st>>>(a);
@@ -816,11 +851,10 @@ int layer_forward(fs_ctx* c, int l) {
         yf, (const float*)w.bqkv, c->rope, (float*)c->q, (float*)kv_plane(c, l, 0),
         (float*)kv_plane(c, l, 1), H, Hkv, hd, f.max_ctx, c->d_rows);
     CK_LAUNCH(c);
-    static bool sattr = false;
-    if (!sattr) {
+    static std::atomic<uint64_t> sattr{0};
+    once_per_device(sattr, c, [] {
       cudaFuncSetAttribute(attn_simple_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      sattr = true;
-    }
+    });
     // scores for up to max_ctx keys (fixed size: the launch is graph-replayed)
     attn_simple_kernel<float><<<dim3(H, FS_MAX_SEG), 128, (size_t)f.max_ctx * 4, c->st>>>(
         (const float*)c->q, (const float*)kv_plane(c, l, 0), (const float*)kv_plane(c, l, 1),
@@ -938,6 +972,93 @@ int sync(fs_ctx* c) {
   return FS_OK;
 }
 
+// ---------------------------------------------------------------- stage transport (a10)
+// One grouped exchange of this rank (R8): send `sw` 4-byte words from
+// sptr to rank+1, receive `rw` words into rptr from rank-1, and broadcast `bw`
+// words at bptr from the last rank to every rank.  Zero counts skip a leg; all
+// ranks agree on the legs because the schedule is replicated.  NCCL: one group
+// (one launch).  Local group: post every outgoing buffer first, then pull every
+// incoming one, then wait for the acknowledgements (no cycle can block).
+int exchange(fs_ctx* c, const void* sptr, size_t sw, void* rptr, size_t rw, void* bptr, size_t bw) {
+  const int p = c->rank, P = c->P;
+  if (P == 1 || (!sw && !rw && !bw)) return FS_OK;
+  if (!c->lg) {
+    CK_NCCL(c, ncclGroupStart());
+    if (sw) CK_NCCL(c, ncclSend(sptr, sw, ncclFloat32, p + 1, c->comm, c->st));
+    if (rw) CK_NCCL(c, ncclRecv(rptr, rw, ncclFloat32, p - 1, c->comm, c->st));
+    if (bw) CK_NCCL(c, ncclBroadcast(bptr, bptr, bw, ncclInt32, P - 1, c->comm, c->st));
+    CK_NCCL(c, ncclGroupEnd());
+    return FS_OK;
+  }
+  fs_local_group* g = c->lg;
+  const bool root = p == P - 1;
+  auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
+  auto fail_tx = [&](const char* why) {
+    c->poisoned = true;
+    c->err = std::string("local transport: ") + why;
+    return FS_ENCCL;
+  };
+  // 1. posts
+  int posts[FS_MAX_STAGES], n_posts = 0;
+  if (sw) posts[n_posts++] = p + 1;
+  if (bw && root)
+    for (int q = 0; q < P - 1; q++) posts[n_posts++] = q;
+  if (n_posts) {
+    CK_CUDA(c, cudaEventRecord(c->ev_ready, c->st));
+    std::lock_guard<std::mutex> lk(g->mu);
+    for (int k = 0; k < n_posts; k++) {
+      auto& ch = g->ch[p][posts[k]];
+      // the last stage only broadcasts, every other stage only sends
+      ch.ptr = root ? bptr : sptr;
+      ch.bytes = 4 * (root ? bw : sw);
+      ch.ready = c->ev_ready;
+      ch.posted++;
+    }
+    g->cv.notify_all();
+  }
+  // 2. pulls (recv from p-1, broadcast from the root)
+  auto pull = [&](int src, void* dst, size_t bytes) -> int {
+    auto& ch = g->ch[src][p];
+    const void* from;
+    cudaEvent_t ready;
+    {
+      std::unique_lock<std::mutex> lk(g->mu);
+      if (!g->cv.wait_until(lk, deadline, [&] { return ch.posted > ch.taken; }))
+        return fail_tx("peer did not post in time");
+      if (ch.bytes != bytes) return fail_tx("peer posted a different size");
+      from = ch.ptr;
+      ready = ch.ready;
+    }
+    CK_CUDA(c, cudaStreamWaitEvent(c->st, ready, 0));
+    CK_CUDA(c, cudaMemcpyAsync(dst, from, bytes, cudaMemcpyDefault, c->st));
+    CK_CUDA(c, cudaEventRecord(c->ev_done[src], c->st));
+    std::lock_guard<std::mutex> lk(g->mu);
+    ch.done = c->ev_done[src];
+    ch.taken++;
+    g->cv.notify_all();
+    return FS_OK;
+  };
+  int rc;
+  // a non-root rank that also sends posted the send first; broadcast and
+  // recv pulls come from different channels ([P-1][p] vs [p-1][p])
+  if (rw && (rc = pull(p - 1, rptr, 4 * rw))) return rc;
+  if (bw && !root && (rc = pull(P - 1, bptr, 4 * bw))) return rc;
+  // 3. acknowledgements: the stream may not overwrite a posted buffer before
+  // the receiver's copy has run
+  for (int k = 0; k < n_posts; k++) {
+    auto& ch = g->ch[p][posts[k]];
+    cudaEvent_t done;
+    {
+      std::unique_lock<std::mutex> lk(g->mu);
+      if (!g->cv.wait_until(lk, deadline, [&] { return ch.taken == ch.posted; }))
+        return fail_tx("peer did not receive in time");
+      done = ch.done;
+    }
+    CK_CUDA(c, cudaStreamWaitEvent(c->st, done, 0));
+  }
+  return FS_OK;
+}
+
 bool check(fs_ctx* c, int* rc) {
   if (!c) {
     *rc = FS_EINVAL;
@@ -947,6 +1068,9 @@ bool check(fs_ctx* c, int* rc) {
     *rc = FS_EPOISONED;
     return false;
   }
+  // the calling thread may not have this context's device current (local
+  // groups drive one context per thread)
+  cudaSetDevice(c->cfg.device);
   return true;
 }
 
@@ -987,7 +1111,8 @@ int fs_init(const fs_config* cfg, fs_ctx** out) {
     return FS_EINVAL;
   }
   if (!cfg->arena || !cfg->stream) return FS_EINVAL;
-  if (cfg->n_stages > 1 && !cfg->nccl_id) return FS_EINVAL;
+  if (cfg->n_stages > 1 && !cfg->nccl_id == !cfg->local_group) return FS_EINVAL;
+  if (cfg->local_group && cfg->local_group->P != cfg->n_stages) return FS_EINVAL;
   fs_ctx* c = new fs_ctx();
   setup_ctx(c, cfg);
   if (cudaSetDevice(cfg->device) != cudaSuccess) {
@@ -1024,7 +1149,25 @@ int fs_init(const fs_config* cfg, fs_ctx** out) {
     delete c;
     return FS_ECUDA;
   }
-  if (c->P > 1) {
+  if (c->P > 1 && cfg->local_group) {
+    fs_local_group* g = cfg->local_group;
+    if (cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming) != cudaSuccess) {
+      delete c;
+      return FS_ECUDA;
+    }
+    for (int q = 0; q < c->P; q++)
+      if (cudaEventCreateWithFlags(&c->ev_done[q], cudaEventDisableTiming) != cudaSuccess) {
+        fs_destroy(c);
+        return FS_ECUDA;
+      }
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->member[c->rank]) {
+      fs_destroy(c);
+      return FS_EINVAL;
+    }
+    g->member[c->rank] = c;
+    c->lg = g;
+  } else if (c->P > 1) {
     ncclUniqueId id;
     memcpy(id.internal, cfg->nccl_id, 128);
     if (ncclCommInitRank(&c->comm, c->P, id, c->rank) != ncclSuccess) {
@@ -1139,17 +1282,11 @@ static int run_chunk_through_pipeline(fs_ctx* c) {
   const int n = c->h_rows->n_rows;
   const int d = c->cfg.d_model;
   if ((rc = upload_rows(c))) return rc;
-  if (c->P > 1 && !c->first) {
-    CK_NCCL(c, ncclRecv(c->x, (size_t)n * d, ncclFloat32, c->rank - 1, c->comm, c->st));
-  }
+  if (c->P > 1 && !c->first && (rc = exchange(c, nullptr, 0, c->x, (size_t)n * d, nullptr, 0))) return rc;
   if ((rc = stage_forward(c, false))) return rc;
-  if (c->P > 1 && !c->last) {
-    CK_NCCL(c, ncclSend(c->x, (size_t)n * d, ncclFloat32, c->rank + 1, c->comm, c->st));
-  }
-  if (c->P > 1) {
-    CK_NCCL(c, ncclBroadcast(c->res, c->res, sizeof(RowResult) * n / 4, ncclInt32, c->P - 1, c->comm,
-                             c->st));
-  }
+  if (c->P > 1 && (rc = exchange(c, c->x, c->last ? 0 : (size_t)n * d, nullptr, 0, c->res,
+                                 sizeof(RowResult) * n / 4)))
+    return rc;
   // h_rows (pinned) is rewritten for the next chunk: the async H2D copy above
   // must have executed first
   return sync(c);
@@ -1309,14 +1446,9 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     const Seg prev = c->slot[p > 0 ? p - 1 : 0];
     const bool recv = p > 0 && prev.valid() && prev.n() > 0;
     const bool send = !c->last && has;
-    if (recv || send || out_rows) {
-      CK_NCCL(c, ncclGroupStart());
-      if (send) CK_NCCL(c, ncclSend(c->x, (size_t)cur.n() * d, ncclFloat32, p + 1, c->comm, c->st));
-      if (recv) CK_NCCL(c, ncclRecv(c->hin, (size_t)prev.n() * d, ncclFloat32, p - 1, c->comm, c->st));
-      if (out_rows)
-        CK_NCCL(c, ncclBroadcast(c->res, c->res, (size_t)outseg.n() * 2, ncclInt32, P - 1, c->comm, c->st));
-      CK_NCCL(c, ncclGroupEnd());
-    }
+    if ((rc = exchange(c, c->x, send ? (size_t)cur.n() * d : 0, c->hin, recv ? (size_t)prev.n() * d : 0,
+                       c->res, out_rows ? (size_t)outseg.n() * 2 : 0)))
+      return rc;
   }
   for (int q = 0; q < P; q++)
     if (c->slot[q].valid()) c->n_cached[q] = std::max(c->n_cached[q], c->slot[q].e);
@@ -1895,8 +2027,28 @@ int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32
   return rc;
 }
 
+int fs_local_group_create(int32_t n_stages, fs_local_group** out) {
+  if (!out) return FS_EINVAL;
+  *out = nullptr;
+  if (n_stages < 2 || n_stages > FS_MAX_STAGES) return FS_EINVAL;
+  fs_local_group* g = new fs_local_group();
+  g->P = n_stages;
+  *out = g;
+  return FS_OK;
+}
+
+void fs_local_group_destroy(fs_local_group* g) { delete g; }
+
 void fs_destroy(fs_ctx* c) {
   if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  if (c->lg) {
+    std::lock_guard<std::mutex> lk(c->lg->mu);
+    if (c->lg->member[c->rank] == c) c->lg->member[c->rank] = nullptr;
+  }
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  for (int q = 0; q < FS_MAX_STAGES; q++)
+    if (c->ev_done[q]) cudaEventDestroy(c->ev_done[q]);
   if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->comm) ncclCommDestroy(c->comm);

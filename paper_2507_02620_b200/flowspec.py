@@ -31,7 +31,7 @@ class fs_config(C.Structure):
                 ("n_stages", i32), ("rank", i32), ("layers_per_stage", C.POINTER(i32)),
                 ("max_ctx", i32), ("max_live", i32), ("max_seg", i32), ("device", i32),
                 ("arena", C.c_void_p), ("arena_bytes", C.c_size_t), ("stream", C.c_void_p),
-                ("nccl_id", C.POINTER(C.c_uint8))]
+                ("nccl_id", C.POINTER(C.c_uint8)), ("local_group", C.c_void_p)]
 
 
 class fs_submit_out(C.Structure):
@@ -66,7 +66,7 @@ class fs_profile(C.Structure):
 EXPORTS = ["fs_layers_per_stage", "fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
-           "fs_last_error", "fs_strerror"]
+           "fs_last_error", "fs_strerror", "fs_local_group_create", "fs_local_group_destroy"]
 EXPORTS.sort()
 
 _lib = None
@@ -101,6 +101,8 @@ def lib():
         L.fs_bench_kernel.argtypes = [P, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.fs_debug_gemm.argtypes = [P, i32, i32, C.POINTER(C.c_float), i32, C.POINTER(C.c_float)]
         L.fs_destroy.argtypes = [P]
+        L.fs_local_group_create.argtypes = [i32, C.POINTER(P)]
+        L.fs_local_group_destroy.argtypes = [P]
         L.fs_last_error.restype = C.c_char_p
         L.fs_last_error.argtypes = [P]
         L.fs_strerror.restype = C.c_char_p
@@ -142,7 +144,7 @@ class Pipeline:
     """One rank of the pipelined tree verifier (same call names as the C-ABI)."""
 
     def __init__(self, shape, n_stages=1, rank=0, max_ctx=4096, max_live=512, max_seg=16,
-                 device=0, layers_per_stage=None, nccl_id=None, stream=None):
+                 device=0, layers_per_stage=None, nccl_id=None, stream=None, local_group=None):
         import torch
         self.torch = torch
         self.L = lib()
@@ -159,9 +161,11 @@ class Pipeline:
         self.cfg.arena_bytes = nbytes
         self.cfg.stream = self.stream.cuda_stream
         self._nid = None
-        if n_stages > 1:
+        if n_stages > 1 and local_group is not None:
+            self.cfg.local_group = local_group
+        elif n_stages > 1:
             if nccl_id is None:
-                raise ValueError("nccl_id required for n_stages > 1")
+                raise ValueError("nccl_id (or local_group) required for n_stages > 1")
             self._nid = (C.c_uint8 * 128)(*bytes(nccl_id))
             self.cfg.nccl_id = C.cast(self._nid, C.POINTER(C.c_uint8))
         h = C.c_void_p()
@@ -262,6 +266,7 @@ class Pipeline:
         self._chk(self.L.fs_query(self.h, FS_Q_STATE, C.byref(s), C.sizeof(s), None), "fs_query")
         P = s.n_stages
         return dict(l_glo=s.l_glo, x_new=s.x_new, live=s.live, n_live=s.n_live, next_id=s.next_id,
+                    rank=s.rank,
                     n_cached=list(s.n_cached[:P]), layers_per_stage=list(s.layers_per_stage[:P]),
                     layer_begin=s.layer_begin, layer_end=s.layer_end,
                     queue=[tuple(s.queue[i]) for i in range(s.n_queue)],
@@ -301,6 +306,103 @@ class Pipeline:
         self._chk(self.L.fs_read_kv(self.h, layer, which, kvh, slot,
                                     out.ctypes.data_as(C.POINTER(C.c_float))), "fs_read_kv")
         return out
+
+
+class LocalPipeline:
+    """A P-stage pipeline inside ONE process: one context per stage (each on its
+    own CUDA stream, all on `devices[p]`, default one device), joined by an
+    fs_local_group so the stage transport is a device copy instead of NCCL
+    (include/flowspec.h).  SPMD as under torchrun: every call is made on every
+    stage with the same host inputs; the collective calls run one host thread
+    per stage.  Results are the last stage's (the one that holds the head)."""
+
+    COLLECTIVE = ("fs_set_prefix", "fs_verify_step")
+
+    def __init__(self, shape, n_stages, max_ctx=4096, max_live=512, max_seg=16, devices=None,
+                 layers_per_stage=None):
+        from concurrent.futures import ThreadPoolExecutor
+        self.L = lib()
+        self.P = n_stages
+        g = C.c_void_p()
+        rc = self.L.fs_local_group_create(n_stages, C.byref(g))
+        if rc != FS_OK:
+            raise FlowSpecError(rc, "fs_local_group_create")
+        self.group = g
+        devices = devices or [0] * n_stages
+        self.stages = [Pipeline(shape, n_stages=n_stages, rank=p, max_ctx=max_ctx, max_live=max_live,
+                                max_seg=max_seg, device=devices[p], layers_per_stage=layers_per_stage,
+                                local_group=g) for p in range(n_stages)]
+        self.shape = shape
+        self.cfg = self.stages[-1].cfg
+        self.pool = ThreadPoolExecutor(max_workers=n_stages)
+
+    @property
+    def last(self):
+        return self.stages[-1]
+
+    def _all(self, name, *a, **kw):
+        if name in self.COLLECTIVE:
+            futs = [self.pool.submit(getattr(st, name), *a, **kw) for st in self.stages]
+            res = [f.result() for f in futs]
+        else:
+            res = [getattr(st, name)(*a, **kw) for st in self.stages]
+        return res[-1]
+
+    def fs_load_random_weights(self, seed):
+        return self._all("fs_load_random_weights", seed)
+
+    def fs_set_prefix(self, tokens, mode=FS_PREFILL, kv_seed=0):
+        return self._all("fs_set_prefix", tokens, mode, kv_seed)
+
+    def fs_submit_segment(self, flags, parent, token, own, l_max, l_top=0):
+        return self._all("fs_submit_segment", flags, parent, token, own, l_max, l_top)
+
+    def fs_verify_step(self):
+        return self._all("fs_verify_step")
+
+    def fs_accept(self):
+        return self._all("fs_accept")
+
+    def fs_prune_and_compact(self, decision):
+        return self._all("fs_prune_and_compact", decision)
+
+    def enable_logits(self, rows_cap=None):
+        self.last.enable_logits(rows_cap)
+
+    decision_dict = staticmethod(Pipeline.decision_dict)
+
+    def state(self):
+        return self.last.state()
+
+    def query(self, what):
+        return self.last.query(what)
+
+    def stage_of_layer(self, layer):
+        for st in self.stages:
+            s = st.state()
+            if s["layer_begin"] <= layer < s["layer_end"]:
+                return st
+        raise ValueError(layer)
+
+    def read_kv(self, layer, which, kvh, slot):
+        return self.stage_of_layer(layer).read_kv(layer, which, kvh, slot)
+
+    def close(self):
+        for st in getattr(self, "stages", []):
+            st.close()
+        self.stages = []
+        if getattr(self, "group", None):
+            self.L.fs_local_group_destroy(self.group)
+            self.group = None
+        if getattr(self, "pool", None):
+            self.pool.shutdown()
+            self.pool = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def layers_per_stage(shape, n_stages):

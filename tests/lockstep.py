@@ -38,6 +38,7 @@ class Stats:
         self.decisions = 0
         self.overrides = 0
         self.committed = []
+        self.kv_rows_checked = 0
 
 
 def compare_tree(gp, op, ancw, where=""):
@@ -64,20 +65,55 @@ def compare_tree(gp, op, ancw, where=""):
     assert np.array_equal(cu_g.view(np.uint32), np.asarray(cu_o, np.float32).view(np.uint32)), where
 
 
+def kv_snapshot(stages):
+    """Device KV rows of every cached draft slot, per stage (its own layers),
+    K and V, first and last kv head: {(layer, which, kvh, S index): row}."""
+    snap = {}
+    for st in stages:
+        s = st.state()
+        nc = s["n_cached"][s["rank"]]
+        hk = {0, st.shape.n_kv_heads - 1}
+        for l in range(s["layer_begin"], s["layer_end"]):
+            for w in (0, 1):
+                for h in hk:
+                    for i in range(nc):
+                        snap[(l, w, h, i)] = (st, s["l_glo"], st.read_kv(l, w, h, s["l_glo"] + i))
+    return snap
+
+
+def check_kv_identity(snap, op):
+    """SURVEY §8(c) "Compaction": after fs_prune_and_compact every retained
+    cached draft row is byte-identical to its pre-compaction row, at slot
+    l_glo_old + r(i) (accepted rows at l_glo_old .. l_glo_new - 1)."""
+    lp = op.last_prune
+    ret = set(lp["i_retain"])
+    n = 0
+    for (l, w, h, i), (st, l_old, row) in snap.items():
+        if i not in ret:
+            continue
+        got = st.read_kv(l, w, h, l_old + lp["rank"][i])
+        assert np.array_equal(got.view(np.uint32), row.view(np.uint32)), ("kv identity", l, w, h, i)
+        n += 1
+    return n
+
+
 def run_lockstep(gp, op, trees_fn, n_rounds, l_max, tol, check_tree=True, check_kv=None,
-                 append_fn=None, max_ticks=10000, bfs=False):
+                 append_fn=None, max_ticks=10000, bfs=False, kv_identity=None, l_top=0):
     """trees_fn(round, op) -> tree dict (parent, token, own); both sides get it.
-    bfs: breadth-first submit order (the w/o-SBD ablation, FS_ORDER_BFS)."""
+    bfs: breadth-first submit order (the w/o-SBD ablation, FS_ORDER_BFS).
+    kv_identity: stage contexts whose KV rows are checked byte-identical across
+    every fs_prune_and_compact.  l_top: keep the top-L_top nodes."""
     stats = Stats()
     ancw = gp.cfg.max_live // 32
     for r in range(n_rounds):
         t = trees_fn(r, op)
         so = op.submit(True, t["parent"], t["token"], t["own"], l_max=l_max,
-                       order_mode="bfs" if bfs else "score")
-        sg = gp.fs_submit_segment(1 | (4 if bfs else 0), t["parent"], t["token"], t["own"], l_max)
+                       order_mode="bfs" if bfs else "score", l_top=l_top)
+        sg = gp.fs_submit_segment(1 | (4 if bfs else 0), t["parent"], t["token"], t["own"], l_max,
+                                  l_top)
         assert sg["order"] == so["order"], ("order", r)
         assert sg["bounds"] == [tuple(b) for b in so["bounds"]], ("bounds", r)
-        if "order" in t and not bfs:
+        if "order" in t and not bfs and not l_top:
             assert so["order"] == list(t["order"]), "generator target order not met"
         if check_tree:
             compare_tree(gp, op, ancw, f"submit r{r}")
@@ -119,8 +155,11 @@ def run_lockstep(gp, op, trees_fn, n_rounds, l_max, tol, check_tree=True, check_
                 assert walked & (flagged | set(do.get("flagged", []))), ("decision", r, got, want)
                 stats.overrides += 1
             stats.committed += do["acc_tokens"]
+            snap = kv_snapshot(kv_identity) if kv_identity else None
             gp.fs_prune_and_compact(want)
             op.prune(want)
+            if snap:
+                stats.kv_rows_checked += check_kv_identity(snap, op)
             if check_tree:
                 compare_tree(gp, op, ancw, f"prune r{r} t{ticks}")
             if check_kv:
