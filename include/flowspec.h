@@ -258,14 +258,17 @@ int fs_get_profile(fs_ctx* ctx, fs_profile* out);
  * stage), 5 = layer-0 attention, 6 = RMSNorm, 7 = whole stage forward.
  * Launches back to back `iters` times on the library stream and returns the
  * mean CUDA-event time per launch in *us and the algorithmic bytes per
- * launch in *bytes.  Overwrites activations (not the KV context). */
+ * launch in *bytes.  Overwrites activations (not the KV context).  Kinds 8-10
+ * (timeline probes, printed to stderr) exist only in a -DFS_DIAG build, which
+ * allocates its probe buffers; the product build allocates no device memory. */
 int fs_bench_kernel(fs_ctx* ctx, int32_t kind, int32_t iters, double* us, double* bytes);
 
 /* GEMM numerics check (layer `layer` of this rank, which = 0 QKV, 1 O,
  * 2 gate/up (interleaved rows), 3 down, 4 head): X (host, n x K fp32, n <=
- * max_seg) is staged as the bf16 hi/lo activation pair, Y (host, n x N_out
- * fp32) receives the raw GEMM output (no epilogue).  bf16 configs only. */
-int fs_debug_gemm(fs_ctx* ctx, int32_t layer, int32_t which, const float* X, int32_t n, float* Y);
+ * max_seg) is staged as the bf16 hi/lo activation pair, Y_dev (DEVICE,
+ * caller-allocated, n x N_out fp32) receives the raw GEMM output (no
+ * epilogue).  Synchronous.  bf16 configs only. */
+int fs_debug_gemm(fs_ctx* ctx, int32_t layer, int32_t which, const float* X, int32_t n, float* Y_dev);
 
 void fs_destroy(fs_ctx* ctx);
 const char* fs_last_error(const fs_ctx* ctx);

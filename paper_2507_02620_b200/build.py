@@ -2,6 +2,8 @@
 
     python -m paper_2507_02620_b200.build          # build if stale
     python -m paper_2507_02620_b200.build --force  # rebuild
+    FS_NVCC_FLAGS="-DFS_DIAG" python -m paper_2507_02620_b200.build --force --out /tmp/diag.so
+        # experiment / diagnostic builds (timeline probes, tuning macros) to a separate file
 """
 import glob
 import os
@@ -41,21 +43,24 @@ def stale():
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, out=None):
+    out = out or SO
     if not force and not stale():
         return SO
     inc, lib = nccl_paths()
     cmd = [NVCC, "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-shared", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", inc,
-           os.path.join(CSRC, "api.cu"), "-o", SO + ".tmp",
+           os.path.join(CSRC, "api.cu"), "-o", out + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    extra = os.environ.get("FS_NVCC_FLAGS", "").split()
+    cmd[1:1] = extra
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv or o is not None, verbose="-v" in sys.argv, out=o))

@@ -1523,6 +1523,7 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
   if (!dcs) return fail(c, FS_EINVAL, "null decision");
   if (!c->live) return fail(c, FS_ESTATE, "no live round");
   if (!dcs->progress || dcs->n_acc < 1 || dcs->n_acc > c->n_live) return fail(c, FS_ESTATE, "no progress");
+  if (dcs->x_new < 0 || dcs->x_new >= c->cfg.vocab) return fail(c, FS_ESTATE, "x_new outside the vocabulary");
   c->acc_ready = false;
   // the decision fs_accept returned from the verify step: its rank map is
   // already on the host (prune_plan_kernel), so no device round trip here
@@ -1730,6 +1731,7 @@ int fs_get_profile(fs_ctx* c, fs_profile* out) {
 int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
   int rc;
   if (!check(c, &rc)) return rc;
+#ifdef FS_DIAG  // timeline diagnostics (build with -DFS_DIAG): probe buffers allocated here
   if (kind == 9 || kind == 10) {
     // diagnostics: phase probes of attention (9) or O-projection GEMM with its
     // residual epilogue (10) launches running alone
@@ -1875,6 +1877,9 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
     *bytes = 0;
     return rc;
   }
+#else
+  if (kind >= 8) return fail(c, FS_EINVAL, "diagnostic kinds need a -DFS_DIAG build");
+#endif
   if (!c->weights || !c->prefixed || iters < 1 || !us || !bytes || kind < 0 || kind > 7)  // 8-10: above
     return fail(c, FS_EINVAL, "bad bench request");
   if (kind <= 5 && !c->bf) return fail(c, FS_EINVAL, "bf16 path only");
@@ -1930,6 +1935,7 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
   }
   cudaEventRecord(b, c->st);
   CK_CUDA(c, cudaEventSynchronize(b));
+#ifdef FS_DIAG
   if (g && getenv("FS_ATT_DEBUG")) {
     const int ncta = 148;
     cudaMalloc(&c->gemm_dbg, sizeof(unsigned long long) * 8 * ncta);
@@ -1972,6 +1978,7 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
     cudaFree(c->att_dbg);
     c->att_dbg = nullptr;
   }
+#endif
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
   cudaEventDestroy(a);
@@ -1981,10 +1988,10 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
   return FS_OK;
 }
 
-int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32_t n, float* Y) {
+int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32_t n, float* Y_dev) {
   int rc;
   if (!check(c, &rc)) return rc;
-  if (!c->bf || !c->weights || !X || !Y || n < 1 || n > c->cfg.max_seg || which < 0 || which > 4 ||
+  if (!c->bf || !c->weights || !X || !Y_dev || n < 1 || n > c->cfg.max_seg || which < 0 || which > 4 ||
       layer < c->L0 || layer >= c->L1 || (which == 4 && !c->last))
     return fail(c, FS_EINVAL, "bad debug gemm request");
   LayerW& w = c->lw[layer - c->L0];
@@ -2012,19 +2019,12 @@ int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32
   c->h_rows->n_rows = n;
   c->h_rows->n_keys = 1;
   if ((rc = upload_rows(c))) return rc;
-  float* out = nullptr;
-  CK_CUDA(c, cudaMalloc(&out, sizeof(float) * (size_t)n * N));
   GemmEpi e = base_epi(c);
   e.mode = EPI_STORE;
-  e.out = out;
+  e.out = Y_dev;
   e.ldo = N;
-  rc = launch_gemm(c, *g, e);
-  if (!rc) {
-    cudaMemcpyAsync(Y, out, sizeof(float) * (size_t)n * N, cudaMemcpyDeviceToHost, c->st);
-    rc = sync(c);
-  }
-  cudaFree(out);
-  return rc;
+  if ((rc = launch_gemm(c, *g, e))) return rc;
+  return sync(c);
 }
 
 int fs_local_group_create(int32_t n_stages, fs_local_group** out) {

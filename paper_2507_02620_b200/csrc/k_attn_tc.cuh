@@ -114,11 +114,15 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
 
   const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
   const int split = blockIdx.x, kvh = blockIdx.y, nsplit = gridDim.x;
+#ifdef FS_DIAG  // timeline probes (diagnostic builds only)
 #define TCA_PROBE(k)                                                                       \
   do {                                                                                     \
     if (a.dbg && threadIdx.x == 64)                                                        \
       a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();          \
   } while (0)
+#else
+#define TCA_PROBE(k) do {} while (0)
+#endif
   TCA_PROBE(0);
   const TickRows* rows = a.rows;
   const int G = a.H / a.Hkv;
@@ -399,10 +403,16 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     mbar_wait(&o_full[mi], 0);
     tc_fence_after();
     TCA_PROBE(8);
-    // every MMA has completed: the Q / K / V buffers stage the warp's 32 rows
-    // so that the workspace write is coalesced (a warp's rows r are
-    // consecutive); rows padded to 132 floats keep the 16-byte stores at 4 wavefronts
+    // this M-tile's MMAs have completed (o_full[mi]); the other M-tile's last
+    // P.V may still be reading V of the final stage.  M-tile 0's staging rows
+    // cover [0, 4*32*132*4) = Q plus K of stage 0, whose last reader (the
+    // final Q.K^T of both M-tiles) finished before any P.V was issued; they
+    // never reach V (static_assert below).  Staging makes the workspace write
+    // coalesced (a warp's rows r are consecutive); rows padded to 132 floats
+    // keep the 16-byte stores at 4 wavefronts.
     constexpr int SLD = 128 + 4;
+    static_assert(MT2 == 1 || 4 * 32 * SLD * 4 <= C::Q_BYTES + 2 * TCA_BOX,
+                  "M-tile 0's output staging would overlap V of stage 0");
     float* stg = reinterpret_cast<float*>(smem) + (size_t)wi * 32 * SLD;
 #pragma unroll
     for (int c = 0; c < 4; c++) {

@@ -222,11 +222,15 @@ FS_DEV unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef FS_DIAG  // timeline probes (diagnostic builds only)
 #define ATT_PROBE(k)                                                               \
   do {                                                                             \
     if (a.dbg && threadIdx.x == 0 && (!a.dbg_ends || (k) == 0 || (k) == 14))      \
       a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();  \
   } while (0)
+#else
+#define ATT_PROBE(k) do {} while (0)
+#endif
 
 // block 128 threads (4 warps); dyn smem: Q [QR][LD] + K,V [KC][LD] + anc rows
 __global__ void __launch_bounds__(128) attn_mma_kernel(AttnArgs a) {

@@ -41,10 +41,14 @@ FS_DEV unsigned long long g_gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef FS_DIAG  // timeline probes (diagnostic builds only)
 #define GEMM_PROBE(k)                                        \
   do {                                                       \
     if (sh.dbg) sh.dbg[(size_t)blockIdx.x * 16 + (k)] = g_gtimer(); \
   } while (0)
+#else
+#define GEMM_PROBE(k) do {} while (0)
+#endif
 
 struct GemmEpi {
   int mode;

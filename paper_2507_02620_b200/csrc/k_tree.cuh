@@ -296,6 +296,9 @@ __global__ void __launch_bounds__(TREE_THREADS) prune_kernel(TreeDev t, const De
   if (!s_err && i < n_acc) {
     int s = s_acc_s[i];
     if (i == 0 ? (s != 0) : (t.par[s] != s_acc_s[i - 1])) atomicExch(&s_err, -3);
+    // only verified nodes can be accepted (R3): an unverified accepted node
+    // would commit KV that later stages never computed
+    if (!t.verified[s]) atomicExch(&s_err, -3);
     s_is_acc[s] = 1;
   }
   if (!s_err && i == 0 && cont && t.par[s_nn] != s_acc_s[n_acc - 1]) s_err = -3;

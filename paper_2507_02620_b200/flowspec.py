@@ -296,10 +296,11 @@ class Pipeline:
 
     def debug_gemm(self, layer, which, X, n_out):
         X = np.ascontiguousarray(X, dtype=np.float32)
-        Y = np.zeros((X.shape[0], n_out), np.float32)
+        Y = self.torch.zeros((X.shape[0], n_out), dtype=self.torch.float32, device=self.arena.device)
         self._chk(self.L.fs_debug_gemm(self.h, layer, which, X.ctypes.data_as(C.POINTER(C.c_float)),
-                                       X.shape[0], Y.ctypes.data_as(C.POINTER(C.c_float))), "fs_debug_gemm")
-        return Y
+                                       X.shape[0], C.cast(Y.data_ptr(), C.POINTER(C.c_float))),
+                  "fs_debug_gemm")
+        return Y.cpu().numpy()
 
     def read_kv(self, layer, which, kvh, slot):
         out = np.zeros(self.shape.head_dim, np.float32)

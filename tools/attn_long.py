@@ -1,4 +1,5 @@
 """Attention HBM bandwidth at the long-context configs (configs[3]
+# timeline kinds 8-10 need a diagnostic build: FS_NVCC_FLAGS=-DFS_DIAG python -m paper_2507_02620_b200.build --force
 13B with a 4096-token context, configs[4] 72B GQA with a 16384-token context),
 on the full per-layer shapes with synthetic-KV prefixes."""
 import os, sys

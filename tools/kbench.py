@@ -1,4 +1,5 @@
 import os, sys, json
+# timeline kinds 8-10 need a diagnostic build: FS_NVCC_FLAGS=-DFS_DIAG python -m paper_2507_02620_b200.build --force
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_02620_b200 import flowspec as F
 from synth import gen
