@@ -2,17 +2,22 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N=1 runs BASELINE.json configs[1] (LLaMA2-7B-shaped bf16, prefix 1024 with a
-real prefill, 64-node draft trees, segments of 16, planted accept path a=4).
-N>1 (torchrun, one rank per GPU) runs the same model as an N-stage pipeline
-(configs[2] planting: a=6, two planted nodes per segment over segments 0-2).
-A step is one SD round: submit the tree, pipeline ticks (verify_step), accept,
+Default (every N): BASELINE.json configs[1] (LLaMA2-7B-shaped bf16, prefix
+1024 with a real prefill, 64-node draft trees, segments of 16, planted accept
+path a=4) -- at N>1 (torchrun, one rank per GPU) the same rounds run as an
+N-stage pipeline, so the per-N values form a strong-scaling curve.  A step is
+one SD round: submit the tree, pipeline ticks (verify_step), accept,
 prune/compact, until the continuous condition fails (§3.1-3.3).
+--workload picks the other configs: cfg3 (configs[2] planting), cfg4
+(configs[3]: 13B, 4096-token synthetic-KV context, scenario S steady
+expansion, a step = one tick), cfg5 (configs[4]: Qwen2-72B, 16384-token
+context, 256-node trees), s7b (7B scenario S).
 
-Draft trees are synthetic: the planted path comes from the model's own greedy
-stream, produced before the timed region by autoregressive decoding through
-the same public API (a stand-in for the paper's draft model, which is out of
-scope).  Weights (13.5 GB) >> L2 (126 MB): every step streams them from HBM.
+Draft trees are synthetic (the paper's draft model is out of scope): the
+planted path is the oracle's greedy stream where one is stored
+(synth/streams/, tools/oracle_stream.py), else the model's own greedy stream
+through the same public API; untimed dry runs check that tree verification
+commits the plan.  Weights >> L2 (126 MB): every tick streams them from HBM.
 """
 import argparse
 import json
@@ -34,18 +39,51 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--shape", default="7b")
-    ap.add_argument("--prefix", type=int, default=1024)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="cfg2 = configs[1] (default at every N), cfg3 = configs[2] planting, "
+                         "cfg4 = configs[3] (13B, scenario S), cfg5 = configs[4] (72B), "
+                         "s7b = 7B scenario S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-attn-long", action="store_true")
     return ap.parse_args()
 
 
-def workload(P):
-    if P == 1:
-        return dict(name="cfg2_7b_p1", ranks=(0, 2, 5, 17, 21))
-    return dict(name=f"cfg3_7b_p{P}", ranks=(0, 3, 9, 18, 25, 33, 40))
+# BASELINE.json configs as bench workloads (SURVEY §8(d) per-config inputs).
+# R = round-based (scenario R: each round commits a+1 tokens, then exits);
+# S = steady expansion (scenario S: one long round, a 16-node batch carrying
+# q planted chain nodes appended after every tick).
+WORKLOADS = {
+    "cfg2": dict(cfg="configs[1]", shape="7b", prefix=1024, mode="prefill", n_nodes=64, depth=6,
+                 l_max=16, max_seg=16, ranks=(0, 2, 5, 17, 21), scenario="R"),
+    "cfg3": dict(cfg="configs[2]", shape="7b", prefix=1024, mode="prefill", n_nodes=64, depth=6,
+                 l_max=16, max_seg=16, ranks=(0, 3, 9, 18, 25, 33, 40), scenario="R"),
+    "cfg4": dict(cfg="configs[3]", shape="13b", prefix=4096, mode="synth", n_nodes=128, depth=6,
+                 l_max=16, max_seg=16, ranks=(0, 1, 2, 17, 18, 33, 34), scenario="S", q=2),
+    "cfg5": dict(cfg="configs[4]", shape="72b", prefix=16384, mode="synth", n_nodes=256, depth=8,
+                 l_max=32, max_seg=32, ranks=(0, 3, 9, 40, 47, 70, 90, 100, 120), scenario="R"),
+    "s7b": dict(cfg="sweep 7B scenario S", shape="7b", prefix=1024, mode="prefill", n_nodes=64,
+                depth=6, l_max=16, max_seg=16, ranks=(0, 1, 2, 17, 18, 33, 34), scenario="S", q=2),
+}
+
+# SURVEY §8(d) "Algorithmic work per verified segment" (bytes; 6.54 TB/s ideal
+# tick at P=1/2/4/8, byte-balanced) -> xi ceilings of the two scenarios
+IDEAL_TICK_MS = {"7b": (2.108, 1.074, 0.557, 0.299), "13b": (4.461, 2.255, 1.153, 0.601),
+                 "72b": (22.69, 11.44, 5.86, 3.07)}
+
+
+def xi_ceiling(wl, P):
+    """Scenario S: q / tick.  Scenario R: (a+1) / (((P-1) + k_exit) * tick) with
+    k_exit = the number of segments the planted path spans."""
+    i = {1: 0, 2: 1, 4: 2, 8: 3}.get(P)
+    if i is None:
+        return None
+    tick = IDEAL_TICK_MS[wl["shape"]][i] * 1e-3
+    if wl["scenario"] == "S":
+        return wl["q"] / tick
+    a = len(wl["ranks"]) - 1
+    k_exit = wl["ranks"][-1] // wl["l_max"] + 1
+    return (a + 1) / (((P - 1) + k_exit) * tick)
 
 
 def peaks():
@@ -144,6 +182,40 @@ def run_round(gp, tree, l_max, tokens_out=None):
             return committed, ticks
 
 
+class SteadyRound:
+    """Scenario S driver: one long round; every tick = verify, accept, prune,
+    then append the next batch (a16).  end() stops appending and drains."""
+
+    def __init__(self, gp, tree, exp, l_max):
+        from paper_2507_02620_b200 import flowspec as F
+        self.F, self.gp, self.exp, self.l_max = F, gp, exp, l_max
+        gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], l_max)
+        self.live = True
+
+    def tick(self, tokens_out=None, append=True):
+        gp = self.gp
+        gp.fs_verify_step()
+        d = gp.fs_accept()
+        c = 0
+        if d.progress:
+            c = d.n_acc
+            if tokens_out is not None:
+                tokens_out += list(d.acc_tokens[:d.n_acc])
+            gp.fs_prune_and_compact(d)
+            PRUNES[0] += 1
+            if not d.cont:
+                self.live = False
+                return c
+        if append:
+            par, tok, own = self.exp.next_batch()
+            gp.fs_submit_segment(self.F.FS_APPEND, par, tok, own, self.l_max)
+        return c
+
+    def end(self, tokens_out=None):
+        while self.live:
+            self.tick(tokens_out, append=False)
+
+
 def greedy_stream(gp, count):
     """AR decode through the API: one-node trees (root only)."""
     from paper_2507_02620_b200 import flowspec as F
@@ -161,36 +233,108 @@ def greedy_stream(gp, count):
     return out
 
 
-def plan_schedule(gp, prefix, ranks, n_rounds, n_nodes, depth, l_max, shape, max_iter=6):
-    """Draft-provider stand-in: trees whose planted path is the model's greedy
-    continuation.  The plan starts as an AR greedy stream; each untimed dry run
-    of all rounds replaces it with the stream tree verification actually
-    commits (a flagged near-tie can make it differ from the AR stream) plus an
-    AR continuation, until a dry run follows its plan.  The timed rounds then
-    replay exactly these trees from the same prefix (deterministic)."""
+def oracle_stream(wl):
+    """The oracle's greedy stream for this model / prompt (tools/oracle_stream.py
+    artifact), or None when none is stored (synthetic-KV configs: a CPU
+    prefill of 13B x 4096 / 72B x 16384 is out of reach)."""
+    path = os.path.join(ROOT, "synth", "streams", f"{wl['shape']}_p{wl['prefix']}.json")
+    if wl["mode"] != "prefill" or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
+
+
+def set_prefix(gp, wl, prefix):
     from paper_2507_02620_b200 import flowspec as F
+    if wl["mode"] == "prefill":
+        return gp.fs_set_prefix(prefix, F.FS_PREFILL)
+    return gp.fs_set_prefix(prefix, F.FS_SYNTH_KV, kv_seed=7)
+
+
+def plan_schedule(gp, wl, prefix, shape, n_rounds, n_ticks, max_iter=6):
+    """Draft-provider stand-in (the paper's draft model is out of scope): trees
+    whose planted path is the greedy continuation.  The plan starts as the
+    oracle's greedy stream when one is stored, else the GPU's own
+    AR stream; each untimed dry run replaces it with the stream tree
+    verification actually commits plus an AR continuation, until a dry run
+    follows its plan.  The timed steps replay exactly these inputs from the same
+    prefix (deterministic).  Returns (inputs, plan record)."""
     from synth import gen
+    ranks = wl["ranks"]
     a = len(ranks) - 1
-    need = n_rounds * (a + 1) + a + 2
-    plan = greedy_stream(gp, need)
-    trees, diverged = [], 0
+    q = wl.get("q", 0)
+    if wl["scenario"] == "R":
+        need = n_rounds * (a + 1) + a + 2
+    else:
+        need = a + q * (n_ticks + 4) + q + 2
+    orc = oracle_stream(wl)
+    info = {"source": "gpu greedy AR through the public API"}
+    if orc is not None and len(orc["stream"]) >= 2:
+        plan = list(orc["stream"])
+        info = {"source": f"oracle greedy stream (synth/streams/{wl['shape']}_p{wl['prefix']}.json)"}
+        if len(plan) < need:
+            set_prefix(gp, wl, prefix)
+            plan = plan + greedy_stream_from(gp, plan, need - len(plan))
+            info["source"] += f" + {need - len(orc['stream'])} gpu AR tokens"
+    else:
+        set_prefix(gp, wl, prefix)
+        plan = greedy_stream(gp, need)
+    first_plan = list(plan)
     for it in range(max_iter):
-        gp.fs_set_prefix(prefix, F.FS_PREFILL)
-        trees, committed, diverged = [], [], 0
-        for r in range(n_rounds):
-            c = len(committed)
-            root = gp.state()["x_new"]
-            if c + a + 2 <= len(plan) and plan[c] == root:
-                t = gen.planted_tree(SEED + r, n_nodes, depth, plan[c:c + a + 2], ranks, shape.vocab)
-            else:  # off plan: unplanted tree rooted at the actual next token
-                diverged += 1
-                t = gen.random_tree(SEED + 7 * r, n_nodes, depth, shape.vocab, root)
-            trees.append(t)
-            run_round(gp, t, l_max, committed)
+        set_prefix(gp, wl, prefix)
+        committed, diverged = [], 0
+        if wl["scenario"] == "R":
+            inputs = []
+            for r in range(n_rounds):
+                c = len(committed)
+                root = gp.state()["x_new"]
+                if c + a + 2 <= len(plan) and plan[c] == root:
+                    t = gen.planted_tree(SEED + r, wl["n_nodes"], wl["depth"], plan[c:c + a + 2], ranks,
+                                         shape.vocab)
+                else:  # off plan: unplanted tree rooted at the actual next token
+                    diverged += 1
+                    t = gen.random_tree(SEED + 7 * r, wl["n_nodes"], wl["depth"], shape.vocab, root)
+                inputs.append(t)
+                run_round(gp, t, wl["l_max"], committed)
+        else:
+            t = gen.planted_tree(SEED, wl["n_nodes"], wl["depth"], plan[:a + 2], ranks, shape.vocab)
+            inputs = (t, plan)
+            sr = SteadyRound(gp, t, gen.SteadyExpansion(SEED + 1, t, plan, q, 16, shape.vocab), wl["l_max"])
+            for _ in range(n_ticks):
+                sr.tick(committed)
+                if not sr.live:
+                    diverged += 1
+                    break
+            sr.end(committed)
+        n = min(len(committed), len(first_plan))
+        mism = [i for i in range(n) if committed[i] != first_plan[i]]
+        if it == 0:
+            info["tokens_checked"] = n
+            info["mismatches_first_dry_run"] = len(mism)
+            if mism and orc is not None and mism[0] < len(orc["margin"]):
+                info["first_mismatch_oracle_margin"] = round(orc["margin"][mism[0]], 5)
         if diverged == 0 and committed == plan[:len(committed)]:
-            return trees, 0, it + 1
+            info["dry_runs"] = it + 1
+            return inputs, info
         plan = committed + greedy_stream(gp, need)
-    return trees, diverged, max_iter
+    info["dry_runs"] = max_iter
+    info["unplanned_steps"] = diverged
+    return inputs, info
+
+
+def greedy_stream_from(gp, plan, count):
+    """AR continuation after the tokens of `plan` (committed through one-node
+    rounds first, so the context matches)."""
+    from paper_2507_02620_b200 import flowspec as F
+    for j in range(1, len(plan)):
+        gp.fs_submit_segment(F.FS_NEW_ROUND, [-1], [plan[j - 1]], [1.0], 1)
+        while True:
+            gp.fs_verify_step()
+            d = gp.fs_accept()
+            if d.progress:
+                gp.fs_prune_and_compact(d)
+                break
+    return greedy_stream(gp, count)[1:]
 
 
 def ours(args):
@@ -212,30 +356,40 @@ def ours(args):
         obj = [F.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    shape = SHAPES[args.shape]
-    wl = workload(P)
+    wl = WORKLOADS[args.workload]
+    shape = SHAPES[wl["shape"]]
     ranks = wl["ranks"]
     a = len(ranks) - 1
-    l_max, n_nodes, depth = 16, 64, 6
+    l_max, n_nodes, depth = wl["l_max"], wl["n_nodes"], wl["depth"]
     W, K = args.warmup, args.steps
-    max_ctx = args.prefix + (W + 2 * K + 4) * (a + 1) + 600
+    S = wl["scenario"] == "S"
+    n_rounds = 0 if S else W + 2 * K
+    n_ticks = W + 2 * K if S else 0
+    grow = (n_rounds * (a + 1)) if not S else (a + wl["q"] * (n_ticks + 4))
+    max_ctx = wl["prefix"] + grow + 1200
     clocks = Clocks(local)   # nvidia-smi needs ~1 s to start sampling
     clocks.start()
-    gp = F.Pipeline(shape, n_stages=P, rank=rank, max_ctx=max_ctx, max_live=512, max_seg=16,
+    gp = F.Pipeline(shape, n_stages=P, rank=rank, max_ctx=max_ctx, max_live=512, max_seg=wl["max_seg"],
                     device=local, nccl_id=nccl_id)
     gp.fs_load_random_weights(SEED)
-    prefix = gen.prefix_tokens(SEED, args.prefix, shape.vocab)
-    gp.fs_set_prefix(prefix, F.FS_PREFILL)
-    n_rounds = W + 2 * K
-    trees, diverged, dry_runs = plan_schedule(gp, prefix, ranks, n_rounds, n_nodes, depth, l_max, shape)
-    gp.fs_set_prefix(prefix, F.FS_PREFILL)
-
-    def round_r(r):
-        return run_round(gp, trees[r], l_max)
-
+    prefix = gen.prefix_tokens(SEED, wl["prefix"], shape.vocab)
+    inputs, plan_info = plan_schedule(gp, wl, prefix, shape, n_rounds, n_ticks)
+    set_prefix(gp, wl, prefix)
     st = gp.stream
+
+    if S:
+        t0_tree, plan = inputs
+        sr = SteadyRound(gp, t0_tree, gen.SteadyExpansion(SEED + 1, t0_tree, plan, wl["q"], 16, shape.vocab),
+                         l_max)
+
+        def step(i):
+            return sr.tick(), 1
+    else:
+        def step(i):
+            return run_round(gp, inputs[i], l_max)
+
     for r in range(W):
-        round_r(r)
+        step(r)
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -246,7 +400,7 @@ def ours(args):
     tokens = ticks = 0
     prunes0 = PRUNES[0]
     for r in range(W, W + K):
-        c, t = round_r(r)
+        c, t = step(r)
         tokens += c
         ticks += t
     prunes = PRUNES[0] - prunes0
@@ -262,14 +416,15 @@ def ours(args):
         dev_ms = float(tt.item())
     value = tokens / (dev_ms / 1e3)
 
-    # e2e: same rounds through the public API, host wall clock, host buffers in / records out
+    # e2e: the next K steps through the public API, host wall clock, host
+    # buffers in (tree arrays) / records out
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e_tokens = 0
     for r in range(W + K, W + 2 * K):
-        c, _ = round_r(r)
+        c, _ = step(r)
         e_tokens += c
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -278,6 +433,8 @@ def ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
     e2e = e_tokens / wall
+    if S:
+        sr.end()
     # keep the same load (one-node verify rounds) until the sampler has seen
     # a few samples since the timed region started
     hold_t0 = time.perf_counter()
@@ -294,34 +451,56 @@ def ours(args):
         dist.barrier()
     clk = clocks.stop()
 
-    # roofline of the dominant kernel (weight-streaming GEMM): CUDA-event pairs
-    # around every GEMM / attention launch over K profiled rounds
+    # roofline of the dominant kernel (weight-streaming GEMM)
     hbm, bf16_tf, peak_src = peaks()
     prof = None
     if not args.no_profile:
-        gp.fs_set_prefix(prefix, F.FS_PREFILL)
+        set_prefix(gp, wl, prefix)
         gp.set_profiling(True)
-        ptree = trees[0]
-        p_t0 = time.perf_counter()
         ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev_a.record(st)
-        run_round(gp, ptree, l_max)
+        if S:
+            sr_p = SteadyRound(gp, t0_tree, gen.SteadyExpansion(SEED + 1, t0_tree, plan, wl["q"], 16,
+                                                                shape.vocab), l_max)
+            for _ in range(W + 4):
+                sr_p.tick()
+            p_ticks = W + 4
+        else:
+            _, p_ticks = run_round(gp, inputs[0], l_max)
         ev_b.record(st)
         torch.cuda.synchronize()
+        if S:
+            sr_p.end()
         step_ms = ev_a.elapsed_time(ev_b)
         gp.set_profiling(False)
         prof = gp.get_profile()
         prof["step_ms"] = step_ms
         # per-launch GEMM time with launches back to back (programmatic overlap
         # between consecutive launches as in the step; the event pairs above
-        # serialise every launch): tick rows of a full 16-row prefill chunk
-        gp.fs_set_prefix(prefix, F.FS_PREFILL)
+        # serialise every launch): tick rows of a full prefill chunk
+        set_prefix(gp, wl, prefix)
         if rank == 0:
             prof["b2b"] = gemm_back_to_back(gp, last=(P == 1))
             prof["attn_b2b"] = min((gp.bench_kernel(5, 20) for _ in range(3)), key=lambda x: x[0])
 
     if rank != 0:
+        gp.close()
         return
+    ceil = xi_ceiling(wl, P)
+    model = {"7b": "LLaMA2-7B-shaped (L32 d4096 H32 ffn11008 V32000)",
+             "13b": "LLaMA2-13B-shaped (L40 d5120 H40 ffn13824 V32000)",
+             "72b": "Qwen2-72B-shaped (L80 d8192 H64/KV8 ffn29568 V152064, q/k/v bias)"}[wl["shape"]]
+    wname = f"{args.workload}_{wl['shape']}_p{P}"
+    if S:
+        desc = (f"{wl['cfg']}: {model} bf16, {P} pipeline stage(s), prefix {wl['prefix']} "
+                f"({'real prefill' if wl['mode'] == 'prefill' else 'synthetic KV'}), {n_nodes}-node initial "
+                f"tree depth {depth}, L_max {l_max}, scenario S: one 16-node batch with q={wl['q']} planted "
+                f"chain nodes appended per tick; a step = one pipeline tick")
+    else:
+        desc = (f"{wl['cfg']}: {model} bf16, {P} pipeline stage(s), prefix {wl['prefix']} "
+                f"({'real prefill' if wl['mode'] == 'prefill' else 'synthetic KV'}), {n_nodes}-node draft "
+                f"tree depth {depth}, L_max {l_max}, planted accept path a={a} (scenario R); a step = one "
+                f"SD round")
     rec = {
         "metric": "accepted tokens/s (pipelined tree verify)",
         "value": round(value, 3),
@@ -336,19 +515,20 @@ def ours(args):
         "dtype": "bf16",
         "data": "synthetic (random-init weights, counter-generated prompt and planted draft trees)",
         "config": {
-            "workload": wl["name"] + f": LLaMA2-7B-shaped bf16, {P} pipeline stage(s), prefix "
-                        f"{args.prefix} (real prefill), {n_nodes}-node draft tree depth {depth}, "
-                        f"L_max {l_max}, planted accept path a={a}",
-            "model": "LLaMA2-7B-shaped (L32 d4096 H32 ffn11008 V32000), random init",
+            "workload": f"{wname} — {desc}",
+            "model": model + ", random init",
             "stages": P,
             "tree_nodes": n_nodes,
             "segment": l_max,
-            "prefix": args.prefix,
-            "l2": "inputs larger than L2: 13.5 GB of weights stream from HBM every step",
+            "prefix": wl["prefix"],
+            "scaling_note": "the same workload at every N (strong scaling: fixed work, P splits the "
+                            "layer stack)",
+            "l2": "inputs larger than L2: the weights stream from HBM every tick",
             "tokens_per_step": tokens / K,
             "ticks_per_step": ticks / K,
-            "planted_path_divergences": diverged,
-            "schedule_dry_runs": dry_runs,
+            "planted_stream": plan_info,
+            "xi_ceiling": round(ceil, 1) if ceil else None,
+            "frac_of_xi_ceiling": round(value / ceil, 4) if ceil else None,
         },
         "clocks": clk,
         "e2e": {"value": round(e2e, 3), "unit": "tok/s",
@@ -363,7 +543,7 @@ def ours(args):
         g_bytes = prof["gemm_bytes"] / max(prof["gemm_launches"], 1)
         ach_ev = g_bytes / (g_ms / 1e3) / 1e9
         b2b = prof["b2b"]
-        n_l = shape.n_layers // P
+        n_l = gp.state()["layer_end"] - gp.state()["layer_begin"]
         cnt = {k: (1 if k == "head" else n_l) for k in b2b}
         b_bytes = sum(cnt[k] * b2b[k]["bytes"] for k in b2b)
         b_us = sum(cnt[k] * b2b[k]["us"] for k in b2b)
@@ -375,24 +555,24 @@ def ours(args):
             "per_kernel": {k: {"us": round(v["us"], 2), "bytes": v["bytes"],
                                "GB/s": round(v["bytes"] / v["us"] / 1e3, 1)} for k, v in b2b.items()},
             "event_pairs": {"achieved": round(ach_ev, 1), "frac": round(ach_ev / hbm, 4),
-                            "note": "event pair around every launch of a profiled round (serialises launches)"},
-            "launches_per_step": prof["gemm_launches"],
+                            "note": "event pair around every launch of a profiled step (serialises launches)"},
+            "launches_per_step": round(prof["gemm_launches"] / max(p_ticks, 1) * (ticks / K)),
             "share_of_step": round(min(1.0, b_us * 1e-3 * (ticks / K) / (dev_ms / K)), 4),
             "attention": {
                 "achieved": round(prof["attn_b2b"][1] / prof["attn_b2b"][0] / 1e3, 1),
                 "us_per_layer": round(prof["attn_b2b"][0], 2),
                 "frac": round(prof["attn_b2b"][1] / prof["attn_b2b"][0] / 1e3 / hbm, 4),
-                "unit": "GB/s", "launches_per_step": prof["attn_launches"],
+                "unit": "GB/s", "launches_per_step": round(prof["attn_launches"] / max(p_ticks, 1) * (ticks / K)),
                 "event_pairs_achieved": round(prof["attn_bytes"] / max(prof["attn_ms"], 1e-9) / 1e6, 1),
                 "share_of_step": round(prof["attn_ms"] / prof["step_ms"], 4)},
             "measured": "GEMM: per launch = CUDA events around 20 back-to-back launches of each "
-                        "weight GEMM (layer 0 of this stage, real epilogues, 16-row tick), weighted "
-                        "by launches per tick; bytes = weights (dominant). Attention: 20 back-to-back launches "
-                        "of layer 0's attention at the bench shape (1024-token context, 16 rows)",
+                        "weight GEMM (layer 0 of this stage, real epilogues, one prefill-chunk tick), "
+                        "weighted by launches per tick; bytes = weights (dominant). Attention: 20 "
+                        "back-to-back launches of layer 0's attention at the bench shape",
         }
     if P == 1 and not args.no_cpu_baseline:
-        rec["cpu_baseline"] = cpu_baseline(shape, trees[0], prefix, ranks, tokens / K, ticks / K,
-                                           n_samples=1)
+        t_first = inputs[0] if not S else t0_tree
+        rec["cpu_baseline"] = cpu_baseline(shape, wl, t_first, prefix, tokens / K, ticks / K)
     gp.close()
     if P == 1 and not args.no_attn_long and "roofline" in rec:
         try:
@@ -463,74 +643,74 @@ def attention_long_context(hbm):
 
 
 # ------------------------------------------------------------------ oracle arm
-def oracle_segment_seconds(shape, tree, prefix, n_samples, n_rows=16):
-    """Time the oracle as it stands verifying segments of the round's tree
-    (synthetic prefix KV of the same length, 16-row segments)."""
+def oracle_pass_seconds(shape, wl, tree, prefix):
+    """Seconds of one oracle pass (as it stands: fp64, weights regenerated) of
+    one L_max-row segment of the step's tree through the whole model at the
+    workload's prefix length (synthetic prefix KV: a CPU prefill is not what
+    is being timed).  Models above 20 B parameters are timed on 1- and
+    2-layer versions of the same shape and extrapolated linearly in the layer
+    count (the oracle's cost per layer is the same at every depth)."""
     from oracle.pipeline import OraclePipeline
-    op = OraclePipeline(shape, SEED, n_stages=1, max_slots=len(prefix) + 600)
-    op.set_prefix(prefix, mode="synth", kv_seed=7)
-    t = dict(tree)
-    t["token"] = list(t["token"])
-    t["token"][0] = op.x_new
-    op.submit(True, t["parent"], t["token"], t["own"], l_max=n_rows)
-    times = []
-    for _ in range(n_samples):
-        if not op.queue:
-            break
+    from synth.configs import reduced
+
+    def one(sh):
+        op = OraclePipeline(sh, SEED, n_stages=1, max_slots=len(prefix) + 600)
+        op.set_prefix(prefix, mode="synth", kv_seed=7)
+        t = dict(tree)
+        t["token"] = list(t["token"])
+        t["token"][0] = op.x_new
+        op.submit(True, t["parent"], t["token"], t["own"], l_max=wl["l_max"])
         t0 = time.perf_counter()
         op.verify_step()
-        times.append(time.perf_counter() - t0)
-    return times
+        return time.perf_counter() - t0
+
+    if shape.n_params <= 20e9:
+        return one(shape), f"one pass of the full {shape.n_layers}-layer model"
+    t1 = one(reduced(wl["shape"], 1))
+    t2 = one(reduced(wl["shape"], 2))
+    est = t1 + (shape.n_layers - 1) * (t2 - t1)
+    return est, (f"1- and 2-layer passes of the same shape ({t1:.1f} s, {t2:.1f} s) extrapolated to "
+                 f"{shape.n_layers} layers")
 
 
-def cpu_baseline(shape, tree, prefix, ranks, tok_per_round, ticks_per_round, n_samples=1):
+def cpu_baseline(shape, wl, tree, prefix, tok_per_step, ticks_per_step):
     threads = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    times = oracle_segment_seconds(shape, tree, prefix, n_samples)
-    t_seg = sum(times) / len(times)
-    segs = ticks_per_round  # P = 1: one segment pass per tick
-    return {"value": round(tok_per_round / (segs * t_seg), 5), "unit": "tok/s", "cores": threads,
+    t_seg, how = oracle_pass_seconds(shape, wl, tree, prefix)
+    return {"value": round(tok_per_step / (ticks_per_step * t_seg), 5), "unit": "tok/s", "cores": threads,
             "kind": "oracle",
-            "sample": f"{len(times)} oracle pass(es) of one 16-row segment through the full "
-                      f"{shape.n_layers}-layer model (weights regenerated, fp64) at prefix "
-                      f"{len(prefix)} (synthetic KV); {t_seg:.2f} s/segment, converted with the "
-                      f"GPU run's {tok_per_round:.2f} tokens and {segs:.2f} segment passes per round"}
+            "sample": f"{how}: one {wl['l_max']}-row segment at prefix {len(prefix)} (synthetic KV, "
+                      f"fp64, weights regenerated); {t_seg:.2f} s/segment, converted with the GPU run's "
+                      f"{tok_per_step:.2f} tokens and {ticks_per_step:.2f} segment passes per step"}
 
 
 def reference(args):
-    """--impl reference: the oracle as it stands, same metric/config, rank 0 only."""
+    """--impl reference: the oracle as it stands, same metric / workload, rank 0
+    only.  Each step = one oracle segment pass; a step of the workload is
+    (tokens per step) over (segment passes per step) of them — scenario R: a+1
+    tokens over the segments the planted path spans; scenario S: q per pass."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from synth import gen
     from synth.configs import SHAPES
-    shape = SHAPES[args.shape]
+    wl = WORKLOADS[args.workload]
+    shape = SHAPES[wl["shape"]]
     P = args.gpus
-    wl = workload(P)
     ranks = wl["ranks"]
     a = len(ranks) - 1
     threads = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    prefix = gen.prefix_tokens(SEED, args.prefix, shape.vocab)
+    prefix = gen.prefix_tokens(SEED, wl["prefix"], shape.vocab)
     stream = [0] + list(range(1, a + 3))
-    tree = gen.planted_tree(SEED, 64, 6, stream, ranks, shape.vocab)
-    from oracle.pipeline import OraclePipeline
-    op = OraclePipeline(shape, SEED, n_stages=1, max_slots=args.prefix + 600)
-    op.set_prefix(prefix, mode="synth", kv_seed=7)
-    tree["token"] = list(tree["token"])
-    tree["token"][0] = op.x_new
-    # one oracle step = one 16-row segment pass; a round of this workload is
-    # (a+1) tokens over 2 segment passes at P=1 (P stages: same passes, no overlap on CPU)
-    tok_per_pass = (a + 1) / (2 if P == 1 else 3)
-    secs = []
+    tree = gen.planted_tree(SEED, wl["n_nodes"], wl["depth"], stream, ranks, shape.vocab)
+    if wl["scenario"] == "S":
+        tok_per_pass = float(wl["q"])
+    else:
+        tok_per_pass = (a + 1) / (ranks[-1] // wl["l_max"] + 1)
+    secs, how = [], ""
     for i in range(args.warmup + args.steps):
-        if not op.queue and not any(s is not None for s in op.slot):
-            op.live = False
-            op._reset_round()
-            op.submit(True, tree["parent"], tree["token"], tree["own"], l_max=16)
-        t0 = time.perf_counter()
-        op.verify_step()
-        dt = time.perf_counter() - t0
+        dt, how = oracle_pass_seconds(shape, wl, tree, prefix)
         if i >= args.warmup:
             secs.append(dt)
     tot = sum(secs)
@@ -540,12 +720,12 @@ def reference(args):
         "value": round(value, 5), "unit": "tok/s", "n_gpus": P, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(secs), 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": wl["name"] + " (oracle, CPU)"},
+        "data": "synthetic", "config": {"workload": f"{args.workload}_{wl['shape']}_p{P} (oracle, CPU)"},
         "cpu_baseline": {"value": round(value, 5), "unit": "tok/s", "cores": threads,
                          "kind": "oracle",
-                         "sample": "each step = one oracle pass of a 16-row segment through the "
-                                   "full model at the workload's prefix length (synthetic KV); "
-                                   f"{tok_per_pass:.2f} accepted tokens per pass as in the round"},
+                         "sample": f"each step = {how} of a {wl['l_max']}-row segment at the workload's "
+                                   f"prefix length (synthetic KV); {tok_per_pass:.2f} accepted tokens per "
+                                   "pass as in the GPU step"},
         "e2e": {"value": round(value, 5), "unit": "tok/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     })

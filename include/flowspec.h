@@ -89,6 +89,10 @@ typedef struct fs_config {
                                devices), the stage transport (a10) is a device
                                copy through the group.  Exactly one of nccl_id /
                                local_group must be set when n_stages > 1. */
+  int32_t sampling;         /* 1: the last stage keeps every verified node's fp32
+                               logits ([max_live][vocab], arena) so that
+                               fs_set_acceptance can switch to stochastic
+                               acceptance; 0: greedy only */
 } fs_config;
 
 typedef struct fs_ctx fs_ctx;
@@ -192,10 +196,35 @@ typedef struct fs_accept_out {
   int32_t n_flagged;         /* walked nodes with top-2 margin < 1e-2 */
   int32_t flagged_ids[FS_MAX_LIVE];
 } fs_accept_out;
+#define FS_ACCEPT_GREEDY 0
+#define FS_ACCEPT_STOCHASTIC 1
+/* Acceptance rule of the following rounds (no live round: FS_ESTATE).
+ * GREEDY (default): child c of v is accepted iff token(c) = argmax of v
+ * (R1).  STOCHASTIC: multi-branch speculative rejection sampling at
+ * temperature `temperature` > 0 ("aligned distribution", Table 1 T=1,
+ * P:461; reading R24): at the walk's node v, p = softmax(logits_v / T) and
+ * q = row node_id(v) of q_dev; children in draw order (node id ascending)
+ * are accepted iff u < p(t)/q(t), else p <- norm(max(p - q, 0)),
+ * q(t) <- 0, q <- norm(q); all rejected: x_new ~ p and the round exits.
+ * u = mix(mix(seed ^ 0x5EED5A3C) ^ (node_id * 2^16 + attempt)) >> 40 / 2^24.
+ * The walk runs in the verify step on the last stage (its logits) and its
+ * decision is broadcast with the row results; fs_accept returns it until the
+ * tree changes.  Nodes whose decision margin (|u - ratio|, or the sample's
+ * distance to a CDF boundary) is below 1e-6 are flagged.
+ * q_dev: DEVICE, caller-owned, [q_rows][vocab] fp32, row = node id of the
+ * round (every node that has children needs its row before that node's
+ * segment is verified); fs_submit_segment fails with FS_ECAPACITY for node
+ * ids >= q_rows.  STOCHASTIC needs cfg.sampling = 1 (FS_ESTATE otherwise).
+ * The prefix's first token x_new stays the argmax (fs_set_prefix). */
+int fs_set_acceptance(fs_ctx* ctx, int32_t mode, float temperature, uint64_t seed,
+                      const float* q_dev, int32_t q_rows);
+
 /* Local (deterministic on replicated state, so every rank computes the same
  * record).  Greedy acceptance + Eq. 2 over all verified nodes (R1,
  * R3): from the root, descend while the child carrying the argmax exists and
- * is verified. */
+ * is verified.  Stochastic mode (fs_set_acceptance): returns the decision the
+ * last verify step took (FS_ESTATE if the tree changed under a verified root
+ * since then). */
 int fs_accept(fs_ctx* ctx, fs_accept_out* out);
 
 /* Local.  Apply a decision (normally fs_accept's; the parity harness may pass

@@ -345,6 +345,30 @@ class OraclePipeline:
         r["flagged"] = [self.node[i] for i in r["acc"] if self.margin[i] < T.MARGIN_FLAG]
         return r
 
+    def accept_stochastic(self, q_of, temperature, seed, flag=None):
+        """Stochastic acceptance (R24, oracle/sampling.py) over the verified
+        nodes: p = softmax(logits / T) of this oracle's own logits, q_of(node
+        id) the draft distribution, children in draw order (node id
+        ascending).  flag: decision-margin threshold for near-threshold flags."""
+        from oracle import sampling as SM
+        if not self.live:
+            return dict(progress=0)
+        kids = {}
+        for s in range(len(self.node)):
+            if self.par[s] >= 0:
+                kids.setdefault(self.par[s], []).append(s)
+        r = SM.accept_walk_stochastic(
+            0, lambda v: sorted(kids.get(v, []), key=lambda c: self.node[c]),
+            lambda s: self.tok[s], lambda s: bool(self.verified[s]), lambda s: self.node[s],
+            lambda s: SM.softmax(self.logits[self.node[s]], temperature),
+            lambda s: q_of(self.node[s]), seed, SM.FLAG if flag is None else flag)
+        if not r["progress"]:
+            return r
+        r["acc_ids"] = [self.node[i] for i in r["acc"]]
+        r["acc_tokens"] = [self.tok[i] for i in r["acc"]]
+        r["n_new_id"] = self.node[r["n_new"]] if r["n_new"] >= 0 else -1
+        return r
+
     # ------------------------------------------------------------ prune
     def prune(self, decision):
         """Collaborative pruning or round exit.

@@ -83,7 +83,7 @@ def branch_step(p, q, child_tokens, u_of):
     return -1, t, min(margin, m)
 
 
-def accept_walk_stochastic(root, children, token, verified, node_id, p_of, q_of, seed):
+def accept_walk_stochastic(root, children, token, verified, node_id, p_of, q_of, seed, flag=FLAG):
     """The walk from the current root (R23: no progress until the root is
     verified).  children(v) -> child nodes of v in draw order; p_of / q_of(v)
     -> base / draft distribution at v.  Returns a dict like the greedy walk's:
@@ -95,7 +95,7 @@ def accept_walk_stochastic(root, children, token, verified, node_id, p_of, q_of,
         kids = children(v)
         i, t, margin = branch_step(p_of(v), q_of(v), [token(c) for c in kids],
                                    lambda a: uniform(seed, node_id(v), a))
-        if margin < FLAG:
+        if margin < flag:
             flagged.append(node_id(v))
         if i < 0:
             return dict(progress=1, acc=acc, x_new=t, n_new=-1, cont=0, flagged=flagged)

@@ -29,6 +29,7 @@
 #include "k_attn_tc.cuh"
 #include "k_gen.cuh"
 #include "k_tree.cuh"
+#include "k_sample.cuh"
 #include "state.cuh"
 
 using namespace fs;
@@ -165,6 +166,16 @@ struct fs_ctx {
   uint64_t launches = 0;
   float* logits_buf = nullptr;
   int logits_cap = 0;
+  // stochastic acceptance (k_sample.cuh): per-S-index logits of verified nodes
+  // (last stage, cfg.sampling), fp64 walk scratch, the broadcast decision
+  float* lstore = nullptr;
+  double *samp_r = nullptr, *samp_q = nullptr;
+  SampleDecision* dec = nullptr;
+  int samp_mode = 0;          // 0 greedy, 1 stochastic
+  double inv_temp = 1.0;
+  uint64_t samp_seed = 0;
+  const float* q_dev = nullptr;
+  int q_rows = 0;
   // profiling: event pairs around GEMM / attention launches
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -387,6 +398,12 @@ size_t carve(fs_ctx* c, char* base) {
   c->ssq = cv.take<float>((size_t)((d + 127) / 128) * 4 * np);
   c->head_part = cv.take<Top2>((size_t)((V + 127) / 128) * np);
   c->res = cv.take<RowResult>(FS_MAX_SEG);
+  c->dec = cv.take<SampleDecision>(1);   // directly after res: one broadcast covers both
+  if (f.sampling && c->last) {
+    c->lstore = cv.take<float>((size_t)f.max_live * V);
+    c->samp_r = cv.take<double>(V);
+    c->samp_q = cv.take<double>(V);
+  }
   c->att_chunk_cap = (f.max_ctx + ATT_KC - 1) / ATT_KC;
   const int G = H / Hkv;
   c->aws_o = c->bf ? cv.take<float>((size_t)c->att_chunk_cap * 4 * Hkv * G * np * ATT_HD) : nullptr;
@@ -884,6 +901,11 @@ int layer_forward(fs_ctx* c, int l) {
   return FS_OK;
 }
 
+// where the head writes fp32 logits: the per-S-index store in stochastic
+// mode (the walk needs every verified node's distribution), else the
+// caller's parity buffer (or nowhere)
+float* head_logits(fs_ctx* c) { return c->samp_mode ? c->lstore : c->logits_buf; }
+
 // final RMSNorm + head + argmax/top-2 on the last stage -> c->res
 int head_forward(fs_ctx* c) {
   const fs_config& f = c->cfg;
@@ -892,7 +914,8 @@ int head_forward(fs_ctx* c) {
     GemmEpi e = norm_input(c);
     e.mode = EPI_HEAD;
     e.head_part = c->head_part;
-    e.logits = c->logits_buf;
+    e.logits = head_logits(c);
+    e.logits_by_s = c->samp_mode ? 1 : 0;
     int rc = launch_gemm(c, c->head, e);
     if (rc) return rc;
     argmax_final_kernel<<<FS_MAX_SEG, 32, 0, c->st>>>(c->head_part, c->head.sh.n_tiles, np, c->d_rows,
@@ -905,7 +928,8 @@ int head_forward(fs_ctx* c) {
     gemm_f32_kernel<<<(V + 127) / 128, 128, 0, c->st>>>((const float*)c->wh, (const float*)c->y, c->yf,
                                                         V, d, c->d_rows);
     CK_LAUNCH(c);
-    argmax_rows_kernel<<<FS_MAX_SEG, 256, 0, c->st>>>(c->yf, V, c->d_rows, c->res, c->logits_buf);
+    argmax_rows_kernel<<<FS_MAX_SEG, 256, 0, c->st>>>(c->yf, V, c->d_rows, c->res, head_logits(c),
+                                                      c->samp_mode ? 1 : 0);
     CK_LAUNCH(c);
   }
   return FS_OK;
@@ -939,7 +963,7 @@ int stage_forward(fs_ctx* c, bool from_hin) {
 // d_rows, so one graph serves every tick); direct launches when profiling
 int tick_forward(fs_ctx* c) {
   if (!c->use_graph || c->prof) return stage_forward(c, true);
-  if (c->fwd_exec && c->fwd_logits != c->logits_buf) {
+  if (c->fwd_exec && c->fwd_logits != head_logits(c)) {
     cudaGraphExecDestroy(c->fwd_exec);
     c->fwd_exec = nullptr;
   }
@@ -955,7 +979,7 @@ int tick_forward(fs_ctx* c) {
     cudaGraphDestroy(g);
     c->fwd_kernels = c->launches - l0;
     c->launches = l0;
-    c->fwd_logits = c->logits_buf;
+    c->fwd_logits = head_logits(c);
   }
   CK_CUDA(c, cudaGraphLaunch(c->fwd_exec, c->st));
   c->launches += c->fwd_kernels;
@@ -1130,6 +1154,10 @@ int fs_init(const fs_config* cfg, fs_ctx** out) {
   c->base = (char*)cfg->arena;
   c->cap = cfg->arena_bytes;
   carve(c, c->base);
+  if ((char*)c->dec != (char*)c->res + sizeof(RowResult) * FS_MAX_SEG) {  // one broadcast covers both
+    delete c;
+    return FS_EINVAL;
+  }
   if (c->bf && !build_maps(c)) {
     delete c;
     return FS_ECUDA;
@@ -1372,6 +1400,7 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   const int base = nr ? 0 : c->next_id;
   if (base + n > c->max_ids) return fail(c, FS_ECAPACITY, "node id space exhausted");
   const int n_keep = (L_top > 0 && L_top < n) ? L_top : n;
+  if (c->samp_mode && base + n > c->q_rows) return fail(c, FS_ECAPACITY, "node id beyond the draft distributions (q_rows)");
   if ((nr ? 0 : c->n_live) + n_keep > c->cfg.max_live) return fail(c, FS_ECAPACITY, "max_live");
   if (c->l_glo + (nr ? 0 : c->n_live) + n_keep > c->cfg.max_ctx) return fail(c, FS_ECAPACITY, "max_ctx");
   SubmitIn* s = c->h_sub;
@@ -1442,12 +1471,44 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
   // with the broadcast of the last stage's row results (one NCCL launch per tick)
   const Seg outseg = c->slot[P - 1];
   const bool out_rows = outseg.valid() && outseg.n() > 0;
+  const bool acc = out_rows && c->live && c->n_live > 0;
+  const bool stoch = c->samp_mode != 0;
+  if (stoch && c->last && out_rows) {
+    // stochastic acceptance needs this stage's logits: commit the rows, run the
+    // walk, and broadcast its decision with the row results
+    post_tick_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->res, outseg.b, outseg.n(), c->d_rec, c->n_live,
+                                                    0, 1e-2f);
+    CK_LAUNCH(c);
+    if (acc) {
+      SampleArgs sa;
+      sa.t = c->tree;
+      sa.lstore = c->lstore;
+      sa.q = c->q_dev;
+      sa.q_rows = c->q_rows;
+      sa.V = c->cfg.vocab;
+      sa.n_live = c->n_live;
+      sa.inv_temp = c->inv_temp;
+      sa.seed = c->samp_seed;
+      sa.flag = 1e-6;
+      sa.r = c->samp_r;
+      sa.qs = c->samp_q;
+      sa.dec = c->dec;
+      sample_walk_kernel<<<1, SAMPLE_THREADS, 0, c->st>>>(sa);
+      CK_LAUNCH(c);
+    }
+    if (c->logits_buf)   // parity copy of this tick's rows
+      CK_CUDA(c, cudaMemcpyAsync(c->logits_buf, c->lstore + (size_t)outseg.b * c->cfg.vocab,
+                                 (size_t)outseg.n() * c->cfg.vocab * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
   if (P > 1) {
     const Seg prev = c->slot[p > 0 ? p - 1 : 0];
     const bool recv = p > 0 && prev.valid() && prev.n() > 0;
     const bool send = !c->last && has;
+    // stochastic: res[FS_MAX_SEG] and the decision that follows it in one broadcast
+    const size_t bw = !out_rows ? 0 : stoch ? (sizeof(RowResult) * FS_MAX_SEG + sizeof(SampleDecision)) / 4
+                                            : (size_t)outseg.n() * 2;
     if ((rc = exchange(c, c->x, send ? (size_t)cur.n() * d : 0, c->hin, recv ? (size_t)prev.n() * d : 0,
-                       c->res, out_rows ? (size_t)outseg.n() * 2 : 0)))
+                       c->res, bw)))
       return rc;
   }
   for (int q = 0; q < P; q++)
@@ -1459,18 +1520,32 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
   }
   if (out_rows) {
     const int n = outseg.n();
-    // commit the rows, then the accept walk over the updated tree and the
-    // prune plan of its decision (fs_accept / fs_prune_and_compact consume them
-    // without another device round trip): one kernel, one read-back
     c->acc_ready = false;
     c->plan_ready = false;
-    const bool acc = c->live && c->n_live > 0;
-    post_tick_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->d_rec, c->n_live,
-                                                    acc ? 1 : 0, 1e-2f);
-    CK_LAUNCH(c);
-    CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
-    c->acc_ready = acc;
-    c->plan_ready = acc;
+    if (stoch) {
+      // commit (the last stage did already) and take the broadcast decision
+      if (!c->last) {
+        post_tick_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->d_rec, c->n_live, 0,
+                                                        1e-2f);
+        CK_LAUNCH(c);
+      }
+      if (acc) {
+        apply_decision_kernel<<<1, 256, 0, c->st>>>(c->tree, c->dec, c->d_rec);
+        CK_LAUNCH(c);
+      }
+      CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+      c->acc_ready = acc;
+    } else {
+      // commit the rows, then the accept walk over the updated tree and the
+      // prune plan of its decision (fs_accept / fs_prune_and_compact consume them
+      // without another device round trip): one kernel, one read-back
+      post_tick_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->res, outseg.b, n, c->d_rec, c->n_live,
+                                                      acc ? 1 : 0, 1e-2f);
+      CK_LAUNCH(c);
+      CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
+      c->acc_ready = acc;
+      c->plan_ready = acc;
+    }
     if ((rc = sync(c))) return rc;
     if (out)
       for (int m = 0; m < n; m++) {
@@ -1501,6 +1576,11 @@ int fs_accept(fs_ctx* c, fs_accept_out* out) {
     CK_LAUNCH(c);
     CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
     if ((rc = sync(c))) return rc;
+    // stochastic decisions are taken by the verify step (the last stage's
+    // logits); with the root verified and no such decision pending, the tree
+    // changed after it (the greedy walk above only tells whether the root is
+    // verified)
+    if (c->samp_mode && c->h_rec->progress) return fail(c, FS_ESTATE, "stochastic decision not pending");
   }
   c->acc_ready = false;
   const TreeRecord* r = c->h_rec;
@@ -1575,6 +1655,12 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
       kv_compact_kernel<32><<<planes, 32, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
     else
       return fail(c, FS_EINVAL, "unsupported head_dim for compaction");
+    CK_LAUNCH(c);
+  }
+  // per-S-index logits of the pruned tree's verified nodes (stochastic mode)
+  if (cont && c->samp_mode && c->lstore) {
+    const int v4 = c->cfg.vocab / 4;
+    lstore_compact_kernel<<<(v4 + 255) / 256, 256, 0, c->st>>>((float4*)c->lstore, v4, c->tree.rank, n_live_old, a);
     CK_LAUNCH(c);
   }
   // pruned S-index prefix: count of I_pr entries below x
@@ -2025,6 +2111,27 @@ int fs_debug_gemm(fs_ctx* c, int32_t layer, int32_t which, const float* X, int32
   e.ldo = N;
   if ((rc = launch_gemm(c, *g, e))) return rc;
   return sync(c);
+}
+
+int fs_set_acceptance(fs_ctx* c, int32_t mode, float temperature, uint64_t seed, const float* q_dev,
+                      int32_t q_rows) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  if (c->live) return fail(c, FS_ESTATE, "round live");
+  if (mode == FS_ACCEPT_GREEDY) {
+    c->samp_mode = 0;
+    return FS_OK;
+  }
+  if (mode != FS_ACCEPT_STOCHASTIC || !(temperature > 0.f) || !q_dev || q_rows < 1)
+    return fail(c, FS_EINVAL, "bad acceptance mode");
+  if (!c->cfg.sampling) return fail(c, FS_ESTATE, "context built without cfg.sampling");
+  if (c->cfg.vocab % 4) return fail(c, FS_EINVAL, "stochastic mode needs vocab % 4 == 0");
+  c->samp_mode = 1;
+  c->inv_temp = 1.0 / (double)temperature;
+  c->samp_seed = seed;
+  c->q_dev = q_dev;
+  c->q_rows = q_rows;
+  return FS_OK;
 }
 
 int fs_local_group_create(int32_t n_stages, fs_local_group** out) {

@@ -957,9 +957,10 @@ __global__ void epi_resid_f32_kernel(const float* Y, float* x, int N, const Tick
 
 // argmax/top-2 of fp32 logits rows; optional copy to the parity buffer
 __global__ void argmax_rows_kernel(const float* Y, int V, const TickRows* rows, RowResult* res,
-                                   float* logits_out) {
+                                   float* logits_out, int logits_by_s) {
   const int m = blockIdx.x;
   if (m >= rows->n_rows) return;
+  if (logits_out && logits_by_s) logits_out += (size_t)rows->s_begin * V;
   Top2 t;
   t.v1 = -INFINITY;
   t.i1 = 0x7fffffff;

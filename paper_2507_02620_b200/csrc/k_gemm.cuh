@@ -70,6 +70,7 @@ struct GemmEpi {
   Top2* head_part;     // [n_tiles][NT]
   float* logits;       // optional [rows][vocab]
   int vocab;
+  int logits_by_s;     // 1: row m goes to logits row rows->s_begin + m (per-S-index store)
   // STORE
   float* out;
   int ldo;
@@ -311,10 +312,12 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     }
   } else if (ep.mode == EPI_HEAD) {
     const bool valid = ng < ep.vocab;
-    if (ep.logits && valid)
+    if (ep.logits && valid) {
+      const size_t r0 = ep.logits_by_s ? (size_t)ep.rows->s_begin : 0;
 #pragma unroll
       for (int j = 0; j < W; j++)
-        if (j < jend) ep.logits[(size_t)(mlo + j) * ep.vocab + ng] = v[j];
+        if (j < jend) ep.logits[(r0 + mlo + j) * ep.vocab + ng] = v[j];
+    }
 #pragma unroll
     for (int j = 0; j < W; j++) {
       Top2 tt;

@@ -19,6 +19,7 @@ FS_MAX_LIVE, FS_MAX_SEG, FS_MAX_STAGES = 512, 64, 8
 FS_PREFILL, FS_SYNTH_KV = 0, 1
 FS_NEW_ROUND, FS_APPEND = 1, 2
 FS_ORDER_BFS = 4   # OR into submit flags: breadth-first order (w/o-SBD ablation)
+FS_ACCEPT_GREEDY, FS_ACCEPT_STOCHASTIC = 0, 1
 FS_Q_STATE, FS_Q_NODE, FS_Q_TOKEN, FS_Q_PARENT, FS_Q_POS, FS_Q_ANC, FS_Q_CU, FS_Q_RETAIN = range(8)
 
 i32 = C.c_int32
@@ -31,7 +32,7 @@ class fs_config(C.Structure):
                 ("n_stages", i32), ("rank", i32), ("layers_per_stage", C.POINTER(i32)),
                 ("max_ctx", i32), ("max_live", i32), ("max_seg", i32), ("device", i32),
                 ("arena", C.c_void_p), ("arena_bytes", C.c_size_t), ("stream", C.c_void_p),
-                ("nccl_id", C.POINTER(C.c_uint8)), ("local_group", C.c_void_p)]
+                ("nccl_id", C.POINTER(C.c_uint8)), ("local_group", C.c_void_p), ("sampling", i32)]
 
 
 class fs_submit_out(C.Structure):
@@ -66,7 +67,7 @@ class fs_profile(C.Structure):
 EXPORTS = ["fs_layers_per_stage", "fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
-           "fs_last_error", "fs_strerror", "fs_local_group_create", "fs_local_group_destroy"]
+           "fs_last_error", "fs_strerror", "fs_local_group_create", "fs_local_group_destroy", "fs_set_acceptance"]
 EXPORTS.sort()
 
 _lib = None
@@ -102,6 +103,7 @@ def lib():
         L.fs_debug_gemm.argtypes = [P, i32, i32, C.POINTER(C.c_float), i32, C.POINTER(C.c_float)]
         L.fs_destroy.argtypes = [P]
         L.fs_local_group_create.argtypes = [i32, C.POINTER(P)]
+        L.fs_set_acceptance.argtypes = [P, i32, C.c_float, C.c_uint64, C.c_void_p, i32]
         L.fs_local_group_destroy.argtypes = [P]
         L.fs_last_error.restype = C.c_char_p
         L.fs_last_error.argtypes = [P]
@@ -123,8 +125,9 @@ def _i32(a):
 
 
 def make_config(shape, n_stages=1, rank=0, max_ctx=4096, max_live=512, max_seg=16, device=0,
-                layers_per_stage=None):
+                layers_per_stage=None, sampling=0):
     c = fs_config()
+    c.sampling = sampling
     for k in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "ffn", "vocab",
               "qkv_bias", "bf16"):
         setattr(c, k, int(getattr(shape, k)))
@@ -144,13 +147,14 @@ class Pipeline:
     """One rank of the pipelined tree verifier (same call names as the C-ABI)."""
 
     def __init__(self, shape, n_stages=1, rank=0, max_ctx=4096, max_live=512, max_seg=16,
-                 device=0, layers_per_stage=None, nccl_id=None, stream=None, local_group=None):
+                 device=0, layers_per_stage=None, nccl_id=None, stream=None, local_group=None,
+                 sampling=0):
         import torch
         self.torch = torch
         self.L = lib()
         self.shape = shape
         self.cfg = make_config(shape, n_stages, rank, max_ctx, max_live, max_seg, device,
-                               layers_per_stage)
+                               layers_per_stage, sampling)
         nbytes = self.L.fs_arena_bytes(C.byref(self.cfg))
         if nbytes == 0:
             raise FlowSpecError(FS_EINVAL, "invalid configuration")
@@ -217,6 +221,13 @@ class Pipeline:
         self.logits = self.torch.zeros((rows_cap, self.shape.vocab), dtype=self.torch.float32,
                                        device=self.arena.device)
         self._chk(self.L.fs_set_logits_buffer(self.h, self.logits.data_ptr(), rows_cap), "logits")
+
+    def fs_set_acceptance(self, mode, temperature=1.0, seed=0, q=None):
+        """q: torch float32 CUDA tensor [q_rows, vocab] (row = node id), kept alive here."""
+        self._q = q
+        ptr = q.data_ptr() if q is not None else None
+        rows = q.shape[0] if q is not None else 0
+        self._chk(self.L.fs_set_acceptance(self.h, mode, temperature, seed, ptr, rows), "fs_set_acceptance")
 
     def fs_verify_step(self):
         out = fs_step_out()
@@ -320,7 +331,7 @@ class LocalPipeline:
     COLLECTIVE = ("fs_set_prefix", "fs_verify_step")
 
     def __init__(self, shape, n_stages, max_ctx=4096, max_live=512, max_seg=16, devices=None,
-                 layers_per_stage=None):
+                 layers_per_stage=None, sampling=0):
         from concurrent.futures import ThreadPoolExecutor
         self.L = lib()
         self.P = n_stages
@@ -332,7 +343,7 @@ class LocalPipeline:
         devices = devices or [0] * n_stages
         self.stages = [Pipeline(shape, n_stages=n_stages, rank=p, max_ctx=max_ctx, max_live=max_live,
                                 max_seg=max_seg, device=devices[p], layers_per_stage=layers_per_stage,
-                                local_group=g) for p in range(n_stages)]
+                                local_group=g, sampling=sampling) for p in range(n_stages)]
         self.shape = shape
         self.cfg = self.stages[-1].cfg
         self.pool = ThreadPoolExecutor(max_workers=n_stages)
@@ -360,6 +371,9 @@ class LocalPipeline:
 
     def fs_verify_step(self):
         return self._all("fs_verify_step")
+
+    def fs_set_acceptance(self, mode, temperature=1.0, seed=0, q=None):
+        return self._all("fs_set_acceptance", mode, temperature, seed, q)
 
     def fs_accept(self):
         return self._all("fs_accept")

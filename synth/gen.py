@@ -151,3 +151,68 @@ def random_tree(seed: int, n_nodes: int, max_depth: int, vocab: int, root_token:
         own.append(np.float32(own_lo + (1.0 - own_lo) * q / 7.0))
     return dict(parent=np.array(parent, np.int32), token=np.array(token, np.int32),
                 own=np.array(own, np.float32))
+
+
+class SteadyExpansion:
+    """Scenario S input (SURVEY §8(d) "Trees", configs[3]): the planted greedy
+    chain continues in appended batches (S_mer = S_pr || S_app) so the
+    pipeline never runs dry.  Every batch holds q chain nodes
+    g_{k+1..k+q} hanging off the current chain tip, plus distractors under the
+    tip, the new chain nodes and earlier batch nodes; sibling tokens stay unique
+    across batches and no distractor under a chain node carries the next chain
+    token, so each verified batch commits exactly q tokens.
+
+    tree      the initial NEW_ROUND tree from planted_tree (its planted chain
+              ends at the tip g_a); stream[j] = g_j for j >= 0."""
+
+    def __init__(self, seed, tree, stream, q=2, batch=16, vocab=32000):
+        self.rng = Rng(seed)
+        self.stream = stream
+        self.q, self.batch, self.vocab = q, batch, vocab
+        par = [int(p) for p in tree["parent"]]
+        tok = [int(t) for t in tree["token"]]
+        self.kids = {}
+        for i, p in enumerate(par):
+            if p >= 0:
+                self.kids.setdefault(p, set()).add(tok[i])
+        self.tip = int(tree["planted_ids"][-1])
+        self.k = len(tree["planted_ids"]) - 1        # tip carries g_k
+        self.next_id = len(par)
+
+    def next_batch(self):
+        """(parent ids, tokens, own) of the next APPEND batch (ids continue at
+        next_id; parents precede children)."""
+        q, base = self.q, self.next_id
+        if self.k + q + 1 >= len(self.stream):
+            raise IndexError("stream exhausted")
+        parent, token, own = [], [], []
+        chain = []
+        p = self.tip
+        for j in range(q):                      # chain g_{k+1} .. g_{k+q}
+            t = self.stream[self.k + 1 + j]
+            self.kids.setdefault(p, set()).add(t)
+            parent.append(p)
+            token.append(t)
+            own.append(np.float32(0.95))
+            chain.append(base + j)
+            p = base + j
+        forbid = {self.tip: self.stream[self.k + 1]}
+        for j in range(q):
+            forbid[chain[j]] = self.stream[self.k + 2 + j]
+        anchors = [self.tip] + chain
+        for i in range(q, self.batch):
+            cand = anchors + [base + j for j in range(q, i)]
+            pid = cand[self.rng.below(len(cand))]
+            kids = self.kids.setdefault(pid, set())
+            while True:
+                t = self.rng.below(self.vocab)
+                if t not in kids and forbid.get(pid) != t:
+                    break
+            kids.add(t)
+            parent.append(pid)
+            token.append(t)
+            own.append(np.float32(0.05 + 0.75 * self.rng.uniform()))
+        self.tip = chain[-1]
+        self.k += q
+        self.next_id = base + self.batch
+        return (np.array(parent, np.int32), np.array(token, np.int32), np.array(own, np.float32))
