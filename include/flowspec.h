@@ -137,6 +137,16 @@ int fs_set_prefix(fs_ctx* ctx, const int32_t* tok, int32_t n, int32_t mode,
  * (Table 2; SPEC S:506 reading).
  * Still topological, so every prefix stays ancestor-closed. */
 #define FS_ORDER_BFS 4
+/* Expansion by tree merging (P:383-392 context-aware expansion; with L_top =
+ * L_se the score-aware expansion of P:399-402): (parent, token, own) is a
+ * tree T_new with parent indices WITHIN T_new (parent[0] = -1, parent[i] <
+ * i), rooted at the current root token.  Nodes whose root path already
+ * exists in the live tree are dropped (path-hash table + exact path check);
+ * the new ones get ids next_id, next_id+1, ... in T_new order and are
+ * appended like an APPEND batch (cumulative-score order in the merged tree,
+ * optional top-L_top of them, own segments: S_mer = S_pr || S_app).
+ * out->merged[i] = node id of T_new node i (existing or new). */
+#define FS_MERGE 8
 typedef struct fs_submit_out {
   int32_t n;                     /* nodes added (after optional top-L) */
   int32_t s_base;                /* S index of the first added node */
@@ -144,6 +154,7 @@ typedef struct fs_submit_out {
   int32_t n_segs;                /* segments enqueued */
   int32_t seg_begin[FS_MAX_LIVE + 1]; /* S-index bounds, n_segs+1 entries */
   int32_t seg_id0;               /* id of the first enqueued segment */
+  int32_t merged[FS_MAX_LIVE];   /* FS_MERGE: node id of every T_new node */
 } fs_submit_out;
 /* Local.  Submit a draft tree (NEW_ROUND) or an appended batch (APPEND) and
  * enqueue it as segments:

@@ -228,6 +228,35 @@ class OraclePipeline:
         self.live = True
         return dict(order=[ids[i] for i in order], bounds=bounds)
 
+    def merge(self, parent_rel, tokens, own, l_max, l_top=0, order_mode="score"):
+        """Tree merging (§3.4 context-aware expansion; with l_top =
+        L_se the score-aware expansion of P:399-402): T_new (parent_rel =
+        parent indices within T_new, node 0 = the current root x_new) is
+        merged into T_pr; the nodes whose path is new are appended as S_app
+        (S_mer = S_pr || S_app), ordered by cumulative score in the merged
+        tree, optionally only the top-l_top of them.  Returns submit()'s dict
+        plus merged = the node id of every T_new node (existing or new)."""
+        if not self.live:
+            raise RuntimeError("no live round")
+        parent_rel = [int(p) for p in parent_rel]
+        tokens = [int(t) for t in tokens]
+        if not parent_rel or parent_rel[0] != -1 or tokens[0] != self.tok[0]:
+            raise ValueError("T_new must be rooted at the current root")
+        for i in range(1, len(parent_rel)):
+            if not (0 <= parent_rel[i] < i):
+                raise ValueError("parent must precede child")
+        new, match = T.merge_new_nodes(self.par, self.tok, parent_rel, tokens)
+        base = self.next_id
+        new_id = {i: base + k for k, i in enumerate(new)}
+        merged = [self.node[match[i]] if match[i] >= 0 else new_id[i] for i in range(len(tokens))]
+        if not new:
+            return dict(order=[], bounds=[], merged=merged)
+        par_ids = [merged[parent_rel[i]] for i in new]
+        out = self.submit(False, par_ids, [tokens[i] for i in new], [own[i] for i in new], l_max,
+                          l_top=l_top, order_mode=order_mode)
+        out["merged"] = merged
+        return out
+
     # ------------------------------------------------------------ verify
     def _rows(self, seg, depth, anc):
         rows = list(range(seg.b, seg.e))

@@ -123,3 +123,31 @@ def prune_sets(acc, n_new, anc, n_live):
 def rank_map(i_retain):
     """Position of each retained index in I_retain (order preserved)."""
     return {i: k for k, i in enumerate(i_retain)}
+
+
+def path_of(parent, token, i):
+    """path_T(n): the token sequence from the root to node i."""
+    p = []
+    while i >= 0:
+        p.append(int(token[i]))
+        i = parent[i]
+    return tuple(reversed(p))
+
+
+def merge_new_nodes(pr_parent, pr_token, new_parent, new_token):
+    """Context-aware expansion, tree merging (§3.4).
+
+    P_pr = {path_Tpr(n) | n in T_pr};  N_new = {n in T_new | path_Tnew(n) not
+    in P_pr}.  Both trees are rooted at the current root x_new (T_pr: S index 0;
+    T_new: index 0).  Returns (N_new as T_new indices in T_new order, match)
+    where match[i] = the T_pr node with the same path, or -1 for new nodes."""
+    P_pr = {}
+    for n in range(len(pr_parent)):
+        P_pr[path_of(pr_parent, pr_token, n)] = n
+    new, match = [], []
+    for i in range(len(new_parent)):
+        m = P_pr.get(path_of(new_parent, new_token, i), -1)
+        match.append(m)
+        if m < 0:
+            new.append(i)
+    return new, match

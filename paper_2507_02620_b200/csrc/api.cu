@@ -142,6 +142,7 @@ struct fs_ctx {
   // tree
   TreeDev tree;
   SubmitIn* d_sub = nullptr;
+  SubmitIn* d_sub2 = nullptr;   // merge: the APPEND batch of T_new's new nodes
   DecisionIn* d_dec = nullptr;
   TreeRecord* d_rec = nullptr;
   TickRows* d_rows = nullptr;
@@ -429,6 +430,7 @@ size_t carve(fs_ctx* c, char* base) {
   t.rank = cv.take<int32_t>(ML);
   t.retain = cv.take<uint32_t>(ML / 32);
   c->d_sub = cv.take<SubmitIn>(1);
+  c->d_sub2 = cv.take<SubmitIn>(1);
   c->d_dec = cv.take<DecisionIn>(1);
   c->d_rec = cv.take<TreeRecord>(1);
   c->d_rows = cv.take<TickRows>(1);
@@ -1388,7 +1390,13 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   if (!check(c, &rc)) return rc;
   if (!c->prefixed) return fail(c, FS_ESTATE, "no prefix");
   const int32_t kind = flags & ~FS_ORDER_BFS;
-  if (kind != FS_NEW_ROUND && kind != FS_APPEND) return fail(c, FS_EINVAL, "bad flags");
+  if (kind != FS_NEW_ROUND && kind != FS_APPEND && kind != FS_MERGE) return fail(c, FS_EINVAL, "bad flags");
+  const bool merge = kind == FS_MERGE;
+  if (merge && parent && n >= 1) {   // T_new: parent indices within T_new, node 0 the root
+    if (parent[0] != -1) return fail(c, FS_EINVAL, "merge: T_new node 0 must be the root");
+    for (int i = 1; i < n; i++)
+      if (parent[i] < 0 || parent[i] >= i) return fail(c, FS_EINVAL, "merge: parent must precede child");
+  }
   if (!parent || !token || !own || n < 1 || n > FS_MAX_LIVE || L_max < 1 || L_max > c->cfg.max_seg ||
       L_top < 0)
     return fail(c, FS_EINVAL, "bad submit arguments");
@@ -1413,18 +1421,24 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   memcpy(s->token, token, sizeof(int32_t) * n);
   memcpy(s->own, own, sizeof(float) * n);
   CK_CUDA(c, cudaMemcpyAsync(c->d_sub, s, sizeof(SubmitIn), cudaMemcpyHostToDevice, c->st));
-  submit_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_sub, c->d_rec, nr ? 0 : c->n_live,
-                                               c->cfg.vocab, c->x_new, nr ? 1 : 0);
+  if (merge) {
+    merge_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_sub, c->d_sub2, c->d_rec, c->n_live, base);
+    CK_LAUNCH(c);
+  }
+  submit_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, merge ? c->d_sub2 : c->d_sub, c->d_rec,
+                                               nr ? 0 : c->n_live, c->cfg.vocab, c->x_new, nr ? 1 : 0);
   CK_LAUNCH(c);
   CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, acc_s), cudaMemcpyDeviceToHost, c->st));
   if ((rc = sync(c))) return rc;
   const TreeRecord* r = c->h_rec;
   if (r->err) return fail(c, r->err == -4 ? FS_ECAPACITY : FS_EINVAL, "submit rejected by validation");
   const int s_base = nr ? 0 : c->n_live;
+  const int n_ids = merge ? r->n_batch : n;   // ids the call consumed
   if (out) {
     out->n = r->n;
     out->s_base = s_base;
     memcpy(out->order, r->order, sizeof(int32_t) * r->n);
+    if (merge) memcpy(out->merged, r->merged, sizeof(int32_t) * n);
     out->n_segs = 0;
     out->seg_id0 = c->seg_counter;
   }
@@ -1443,7 +1457,7 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
     out->seg_begin[k] = s_base + r->n;
   }
   c->n_live = r->n_live;
-  c->next_id = base + n;
+  c->next_id = base + n_ids;
   c->live = 1;
   return FS_OK;
 }

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
   const int i = threadIdx.x;
   const int n = in->n;
   const int base = in->base_id;
+  if (n < 0) return;   // the merge kernel rejected the batch (rec->err set)
   if (i == 0) s_err = 0;
   __syncthreads();
   int p = 0, tok = 0, id = base + i;
@@ -187,6 +188,141 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
     rec->err = 0;
     rec->n = n_keep;
     rec->n_live = n_live + n_keep;
+  }
+}
+
+// ---------------------------------------------------------------- merge (f4)
+// Context-aware tree expansion (§3.4): T_new, rooted at the current
+// root, is merged into the live tree T_pr.  A node of T_new is new iff its
+// root path is not a path of T_pr (N_new = {n | path(n) not in P_pr}).  As in
+// the paper, P_pr is a hash table of path hashes, here in shared memory
+// (h(root) = mix(K ^ token), h(n) = mix(h(parent) ^ (token+1) * C), open
+// addressing); a hit is confirmed by comparing the two root paths token by
+// token, so a hash collision cannot merge distinct paths.  Output: the APPEND
+// batch of the new nodes in T_new order (parents mapped to live ids or to the
+// batch's new ids base + rank) for submit_kernel, which orders it by
+// cumulative score, applies top-L_se (score-aware expansion) and
+// enqueues S_app (S_mer = S_pr || S_app).
+FS_DEV uint64_t path_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+FS_DEV uint64_t path_step(uint64_t h_parent, int32_t tok) {
+  return path_mix(h_parent ^ ((uint64_t)(tok + 1) * 0xD1B54A32D192ED03ull)) | 1ull;   // 0 = empty slot
+}
+constexpr int MERGE_SLOTS = 2048;
+
+__global__ void __launch_bounds__(TREE_THREADS) merge_kernel(TreeDev t, const SubmitIn* in, SubmitIn* out,
+                                                             TreeRecord* rec, int32_t n_live, int32_t base) {
+  __shared__ unsigned long long s_hpr[MAXLIVE];
+  __shared__ unsigned long long s_hnew[MAXLIVE];
+  __shared__ int s_ok_pr[MAXLIVE];
+  __shared__ int s_ok_new[MAXLIVE];
+  __shared__ unsigned long long s_key[MERGE_SLOTS];
+  __shared__ int s_val[MERGE_SLOTS];
+  __shared__ int s_match[MAXLIVE];
+  __shared__ int s_rank[MAXLIVE];
+  __shared__ int s_warp[TREE_THREADS / 32 + 1];
+  __shared__ int s_err;
+  const int i = threadIdx.x;
+  const int n = in->n;
+  if (i == 0) s_err = (n < 1 || in->parent[0] != -1 || n_live < 1 || in->token[0] != t.token[0]) ? -1 : 0;
+  for (int k = i; k < MERGE_SLOTS; k += TREE_THREADS) s_key[k] = 0ull;
+  if (i < MAXLIVE) {
+    s_ok_pr[i] = 0;
+    s_ok_new[i] = 0;
+  }
+  __syncthreads();
+  if (s_err) {
+    if (i == 0) {
+      rec->err = -1;
+      out->n = -1;
+    }
+    return;
+  }
+  // path hashes of both trees, level-synchronous (parents precede children)
+  while (true) {
+    int prog_pr = 0, prog_new = 0;
+    if (i < n_live && !s_ok_pr[i]) {
+      const int p = t.par[i];
+      if (p < 0 || s_ok_pr[p]) {
+        s_hpr[i] = p < 0 ? path_step(0x5A3C5EEDull, t.token[i]) : path_step(s_hpr[p], t.token[i]);
+        prog_pr = 1;
+      }
+    }
+    if (i < n && !s_ok_new[i]) {
+      const int p = in->parent[i];
+      if (p < 0 || s_ok_new[p]) {
+        s_hnew[i] = p < 0 ? path_step(0x5A3C5EEDull, in->token[i]) : path_step(s_hnew[p], in->token[i]);
+        prog_new = 1;
+      }
+    }
+    __syncthreads();
+    if (prog_pr) s_ok_pr[i] = 1;
+    if (prog_new) s_ok_new[i] = 1;
+    if (!__syncthreads_or(prog_pr | prog_new)) break;
+  }
+  // P_pr: hash table of T_pr's path hashes -> S index
+  if (i < n_live) {
+    const unsigned long long h = s_hpr[i];
+    for (int k = 0; k < MERGE_SLOTS; k++) {
+      const int slot = (int)((h + k) & (MERGE_SLOTS - 1));
+      const unsigned long long prev = atomicCAS(&s_key[slot], 0ull, h);
+      if (prev == 0ull) {
+        s_val[slot] = i;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  // N_new: lookup + exact path comparison of every candidate with the same hash
+  int m = -1;
+  if (i < n) {
+    const unsigned long long h = s_hnew[i];
+    for (int k = 0; k < MERGE_SLOTS && m < 0; k++) {
+      const int slot = (int)((h + k) & (MERGE_SLOTS - 1));
+      const unsigned long long key = s_key[slot];
+      if (key == 0ull) break;
+      if (key != h) continue;
+      int a = i, b = s_val[slot];
+      while (a >= 0 && b >= 0 && in->token[a] == t.token[b]) {
+        a = in->parent[a];
+        b = t.par[b];
+      }
+      if (a < 0 && b < 0) m = s_val[slot];
+    }
+    s_match[i] = m;
+  }
+  if (i == 0 && s_match[0] != 0) s_err = -1;   // (i == 0 wrote s_match[0] above)
+  int n_new;
+  const int r = block_excl_count(i < n && m < 0, s_warp, &n_new);
+  if (i < n) s_rank[i] = r;
+  __syncthreads();
+  if (s_err) {
+    if (i == 0) {
+      rec->err = -1;
+      out->n = -1;
+    }
+    return;
+  }
+  if (i < n) {
+    rec->merged[i] = m >= 0 ? t.node[m] : base + r;
+    if (m < 0) {
+      const int p = in->parent[i];
+      out->parent[r] = s_match[p] >= 0 ? t.node[s_match[p]] : base + s_rank[p];
+      out->token[r] = in->token[i];
+      out->own[r] = in->own[i];
+    }
+  }
+  if (i == 0) {
+    out->n = n_new;
+    out->flags = FS_APPEND | (in->flags & FS_ORDER_BFS);
+    out->l_top = in->l_top;
+    out->l_max = in->l_max;
+    out->base_id = base;
+    rec->n_batch = n_new;
   }
 }
 

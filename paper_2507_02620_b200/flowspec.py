@@ -19,6 +19,7 @@ FS_MAX_LIVE, FS_MAX_SEG, FS_MAX_STAGES = 512, 64, 8
 FS_PREFILL, FS_SYNTH_KV = 0, 1
 FS_NEW_ROUND, FS_APPEND = 1, 2
 FS_ORDER_BFS = 4   # OR into submit flags: breadth-first order (w/o-SBD ablation)
+FS_MERGE = 8       # submit kind: merge a tree rooted at the current root (f4 expansion)
 FS_ACCEPT_GREEDY, FS_ACCEPT_STOCHASTIC = 0, 1
 FS_Q_STATE, FS_Q_NODE, FS_Q_TOKEN, FS_Q_PARENT, FS_Q_POS, FS_Q_ANC, FS_Q_CU, FS_Q_RETAIN = range(8)
 
@@ -37,7 +38,7 @@ class fs_config(C.Structure):
 
 class fs_submit_out(C.Structure):
     _fields_ = [("n", i32), ("s_base", i32), ("order", i32 * FS_MAX_LIVE), ("n_segs", i32),
-                ("seg_begin", i32 * (FS_MAX_LIVE + 1)), ("seg_id0", i32)]
+                ("seg_begin", i32 * (FS_MAX_LIVE + 1)), ("seg_id0", i32), ("merged", i32 * FS_MAX_LIVE)]
 
 
 class fs_step_out(C.Structure):
@@ -213,8 +214,10 @@ class Pipeline:
         self._chk(self.L.fs_submit_segment(self.h, flags, pp, pt, o.ctypes.data_as(C.POINTER(C.c_float)),
                                            len(p), l_top, l_max, C.byref(out)), "fs_submit_segment")
         bounds = [(out.seg_begin[k], out.seg_begin[k + 1]) for k in range(out.n_segs)]
-        return dict(order=list(out.order[:out.n]), s_base=out.s_base, bounds=bounds,
-                    seg_id0=out.seg_id0)
+        r = dict(order=list(out.order[:out.n]), s_base=out.s_base, bounds=bounds, seg_id0=out.seg_id0)
+        if (flags & ~FS_ORDER_BFS) == FS_MERGE:
+            r["merged"] = list(out.merged[:len(p)])
+        return r
 
     def enable_logits(self, rows_cap=None):
         rows_cap = rows_cap or self.cfg.max_seg

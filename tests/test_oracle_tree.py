@@ -235,3 +235,102 @@ def test_bfs_equals_score_order_on_a_chain():
     cu = T.cumulative_scores(par, [1.0, 0.9, 0.8, 0.7, 0.6])
     ids = list(range(5))
     assert T.bfs_order(T.depth_of(par), ids) == T.score_order(cu, ids) == ids
+
+
+# ------------------------------------------------------------------ f4 merge
+def _tree_paths(parent, token):
+    """Brute force: every node's root path, walked independently of oracle/tree.py."""
+    out = []
+    for i in range(len(parent)):
+        p, j = [], i
+        while j >= 0:
+            p.insert(0, int(token[j]))
+            j = int(parent[j])
+        out.append(tuple(p))
+    return out
+
+
+def _overlapping_trees(seed, vocab=6):
+    """T_pr and T_new rooted at the same token with a small vocabulary, so many
+    paths coincide."""
+    a = gen.random_tree(seed, 25, 4, vocab, 3)
+    b = gen.random_tree(seed + 1000, 25, 4, vocab, 3)
+    return a, b
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_merge_path_set_is_union(seed):
+    """Tree merging: after merging, the tree holds every path of
+    T_pr and T_new exactly once; S_pr stays at the front in its order; every
+    T_new node maps to the node with its path."""
+    from oracle.pipeline import OraclePipeline
+    from synth.configs import SHAPES
+    a, b = _overlapping_trees(seed)
+    op = OraclePipeline(SHAPES["tiny"], 1, n_stages=1, max_slots=256)
+    op.x_new, op.l_glo = 3, 10
+    op.submit(True, a["parent"], a["token"], a["own"], l_max=8)
+    before_nodes = list(op.node)
+    out = op.merge(b["parent"], b["token"], b["own"], l_max=8)
+    P_a = set(_tree_paths(a["parent"], a["token"]))
+    P_b = set(_tree_paths(b["parent"], b["token"]))
+    paths = _tree_paths(op.par, op.tok)
+    assert len(paths) == len(set(paths)) and set(paths) == P_a | P_b
+    assert op.node[:len(before_nodes)] == before_nodes            # S_mer = S_pr || S_app
+    assert len(op.node) == len(before_nodes) + len(P_b - P_a)
+    bp = _tree_paths(b["parent"], b["token"])
+    for i, nid in enumerate(out["merged"]):
+        assert paths[op.id2s[nid]] == bp[i]
+    # appended nodes come after their parents (ancestor-closed prefixes)
+    for s in range(len(op.node)):
+        assert op.par[s] < s
+
+
+def test_merge_special_cases():
+    from oracle.pipeline import OraclePipeline
+    from synth.configs import SHAPES
+    a = gen.random_tree(5, 20, 4, 50, 7)
+    op = OraclePipeline(SHAPES["tiny"], 1, n_stages=1, max_slots=256)
+    op.x_new, op.l_glo = 7, 10
+    op.submit(True, a["parent"], a["token"], a["own"], l_max=8)
+    n0 = len(op.node)
+    # T_new == T_pr: nothing new
+    out = op.merge(a["parent"], a["token"], a["own"], l_max=8)
+    assert out["order"] == [] and len(op.node) == n0 and out["merged"] == list(range(20))
+    # a chain whose first token is new below the root: all of it is appended
+    toks = [7] + [t for t in range(60, 64)]
+    out = op.merge([-1, 0, 1, 2, 3], toks, [1.0, 0.9, 0.9, 0.9, 0.9], l_max=8)
+    assert len(out["order"]) == 4 and len(op.node) == n0 + 4
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_score_aware_top_l_is_score_prefix_of_new_nodes(seed):
+    """Score-aware expansion: of the nodes not yet in T, the top-L_se
+    by cumulative score are appended; the kept set is closed under parents."""
+    from oracle.pipeline import OraclePipeline
+    from synth.configs import SHAPES
+    a, b = _overlapping_trees(seed + 50, vocab=8)
+    op = OraclePipeline(SHAPES["tiny"], 1, n_stages=1, max_slots=256)
+    op.x_new, op.l_glo = 3, 10
+    op.submit(True, a["parent"], a["token"], a["own"], l_max=8)
+    n0 = len(op.node)
+    cu_pr = {op.node[s]: float(c) for s, c in enumerate(op.cu())}
+    new, _ = T.merge_new_nodes(op.par, op.tok, b["parent"], b["token"])
+    out = op.merge(b["parent"], b["token"], b["own"], l_max=8, l_top=5)
+    kept = len(out["order"])
+    assert kept == min(5, len(new)) and len(op.node) == n0 + kept
+    # brute force: Eq. 1 of every new node in the merged tree (fp32 products
+    # along T_new, starting from the matched T_pr ancestor's score)
+    P_a = {p: i for i, p in enumerate(_tree_paths(a["parent"], a["token"]))}
+    bp = _tree_paths(b["parent"], b["token"])
+    cu_a = T.cumulative_scores(a["parent"], a["own"])
+    cu_b = {}
+    for i in range(len(bp)):
+        if bp[i] in P_a:
+            cu_b[i] = np.float32(cu_a[P_a[bp[i]]])
+        else:
+            cu_b[i] = np.float32(cu_b[int(b["parent"][i])] * np.float32(b["own"][i]))
+    cand = sorted((i for i in range(len(bp)) if bp[i] not in P_a), key=lambda i: (-float(cu_b[i]), i))
+    want = {bp[i] for i in cand[:5]}
+    got = set(_tree_paths(op.par, op.tok)[n0:])
+    assert got == want
+    assert all(op.par[s] < s for s in range(len(op.node)))
