@@ -27,6 +27,7 @@
 #include "k_fwd.cuh"
 #include "k_gemm.cuh"
 #include "k_attn_tc.cuh"
+#include "k_attn_mha.cuh"
 #include "k_gen.cuh"
 #include "k_tree.cuh"
 #include "k_sample.cuh"
@@ -72,6 +73,7 @@ struct LayerW {
   void *g1 = nullptr, *g2 = nullptr;
   GemmOp qkv, o, gu, dn;
   CUtensorMap tk, tv;   // this layer's K / V cache planes [Hkv * max_ctx][128] (GQA tcgen05 attention)
+  CUtensorMap mk, mv;   // the same planes in 64-key boxes (MHA attention, TMA ring)
 };
 
 }  // namespace
@@ -102,6 +104,7 @@ struct fs_ctx {
   int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536, gemm_ctas = 2;
   int att_dbg_ends = 0;
   int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
+  int mha_nsplit[3] = {0, 0, 0};   // TMA MHA attention: splits per m-tile count (SM-count sized)
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   fs_local_group* lg = nullptr;           // single-process stage transport (else NCCL)
@@ -503,6 +506,8 @@ bool build_maps(fs_ctx* c) {
     const uint64_t kv_rows = (uint64_t)Hkv * f.max_ctx;
     ok &= encode_map(&w.tk, kv_plane(c, l, 0), hd, kv_rows, 64, 128);
     ok &= encode_map(&w.tv, kv_plane(c, l, 1), hd, kv_rows, 64, 128);
+    ok &= encode_map(&w.mk, kv_plane(c, l, 0), hd, kv_rows, 64, ATT_SUB);
+    ok &= encode_map(&w.mv, kv_plane(c, l, 1), hd, kv_rows, 64, ATT_SUB);
   }
   if (c->last) {
     ok &= encode_wmap(&c->head.ta, c->wh, d, f.vocab);
@@ -696,8 +701,60 @@ int launch_attention(fs_ctx* c, int l) {
     const int G = H / Hkv, QR = G * np, MT = QR / 16;
     const int KS = MT >= 4 ? 1 : 4 / MT;
     const int n_keys = c->h_rows->n_keys;
-    if (MT <= 2) {
-      // MHA path: key splits of one kv head form a cluster (DSMEM merge), PDL launch
+    if (MT <= 2 && hd == ATT_HD && !getenv("FS_MHA_CP_ASYNC")) {
+      // MHA path: TMA-staged K/V ring, splits sized to fill every SM slot,
+      // partials merged by attn_combine_kernel (programmatic launch)
+      const size_t smem = mha_tma_smem(np, c->ancw);
+      static std::atomic<uint64_t> tattr{0};
+      once_per_device(tattr, c, [] {   // the largest any context needs (npad 64, max_live 512)
+        const int mx = (int)mha_tma_smem(64, FS_MAX_LIVE / 32);
+        cudaFuncSetAttribute(attn_mha_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(attn_mha_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+      });
+      if (c->mha_nsplit[MT] == 0) {
+        int occ = 0;
+        if ((MT == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<16>, MHA_THREADS, smem)
+                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<32>, MHA_THREADS, smem)) !=
+                cudaSuccess ||
+            occ < 1) {
+          cudaGetLastError();
+          occ = 1;
+        }
+        int ns = std::max(1, occ * c->n_sms / Hkv);
+        ns = std::min(ns, (f.max_ctx + ATT_SUB - 1) / ATT_SUB);   // at least one sub-chunk of keys each
+        ns = std::min(ns, c->att_chunk_cap * 4);                   // workspace capacity
+        ns = std::min(ns, 8);   // the combine loads 8 splits per round trip (9 splits: 11.4 vs 10.0 us, 7B)
+        if (getenv("FS_ATT_NSPLIT")) ns = std::max(1, std::min(ns, atoi(getenv("FS_ATT_NSPLIT"))));
+        c->mha_nsplit[MT] = ns;
+      }
+      const int nsplit = c->mha_nsplit[MT];
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(nsplit, Hkv);
+      lc.blockDim = dim3(MHA_THREADS);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = c->st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 * 3);
+      if (MT == 1)
+        cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<16>, c->lw[l].mk, c->lw[l].mv, a);
+      else
+        cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<32>, c->lw[l].mk, c->lw[l].mv, a);
+      CK_LAUNCH(c);
+      cudaLaunchConfig_t cc = {};
+      cc.gridDim = dim3(np, H);
+      cc.blockDim = dim3(ATT_HD);
+      cc.stream = c->st;
+      cc.attrs = at;
+      cc.numAttrs = 1;
+      cudaLaunchKernelEx(&cc, attn_combine_kernel, a, (bf16*)c->att, 1, nsplit);
+      prof_end(c, api);
+      CK_LAUNCH(c);
+    } else if (MT <= 2) {
+      // MHA path (FS_MHA_CP_ASYNC): key splits of one kv head form a cluster (DSMEM merge), PDL launch
       AttnMhaArgs ma;
       ma.a = a;
       ma.out = (bf16*)c->att;

@@ -529,10 +529,24 @@ FS_DEV void mha_load_q(MhaWarp<KPW>& w, const bf16* sQ, int lane) {
             sQ + (size_t)(w.mt * 16 + (lane & 15)) * ATT_LD + kk * 16 + (lane >> 4) * 8);
 }
 
+// address of the 8-element (16-byte) chunk at (row, col) of a K or V tile:
+// padded rows (cp.async staging) or the TMA SWIZZLE_128B layout of two
+// [rows][64] boxes (hd 0-63, 64-127; box stride rows * 128 B), where the
+// 16-byte chunk index is XORed with the row's index mod 8
+template <bool SW, int ROWS>
+FS_DEV const bf16* kv_chunk(const bf16* base, int row, int col) {
+  if constexpr (SW) {
+    const int off = (col >> 6) * ROWS * 128 + row * 128 + ((((col & 63) >> 3) ^ (row & 7)) << 4);
+    return reinterpret_cast<const bf16*>(reinterpret_cast<const char*>(base) + off);
+  } else {
+    return base + (size_t)row * ATT_LD + col;
+  }
+}
+
 // one 64-key sub-chunk (keys kbase..kbase+63 in sK / sV): the warp's KPW keys,
 // tree mask unless every key is context of every live row, online softmax, P V
-// with P as a bf16 hi/lo pair (R18)
-template <int KPW>
+// with P as a bf16 hi/lo pair (R18).  SW: sK / sV in the TMA swizzled layout
+template <int KPW, bool SW = false>
 FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, const bf16* sV, int kbase,
                          int kend, int ctx_min, int l_glo, int n_rows, const uint32_t* sAnc, int lane) {
   constexpr int NT8 = KPW / 8;
@@ -547,7 +561,7 @@ FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, con
 #pragma unroll
     for (int j = 0; j < NT8; j++) {
       uint32_t b0, b1;
-      ldsm_x2(b0, b1, sK + (size_t)(kb + j * 8 + (lane & 7)) * ATT_LD + kk * 16 + ((lane >> 3) & 1) * 8);
+      ldsm_x2(b0, b1, kv_chunk<SW, ATT_SUB>(sK, kb + j * 8 + (lane & 7), kk * 16 + ((lane >> 3) & 1) * 8));
       mma_bf16_16816(sacc[j], w.qf[kk][0], w.qf[kk][1], w.qf[kk][2], w.qf[kk][3], b0, b1);
     }
   }
@@ -625,7 +639,7 @@ FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, con
 #pragma unroll
     for (int j = 0; j < 16; j++) {
       uint32_t b0, b1;
-      ldsm_x2_t(b0, b1, sV + (size_t)(kb + kk * 16 + (lane & 15)) * ATT_LD + j * 8);
+      ldsm_x2_t(b0, b1, kv_chunk<SW, ATT_SUB>(sV, kb + kk * 16 + (lane & 15), j * 8));
       mma_bf16_16816(w.oacc[j], ph[0], ph[1], ph[2], ph[3], b0, b1);
       mma_bf16_16816(w.oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
     }

@@ -8,7 +8,7 @@ from paper_2507_02620_b200 import flowspec as F
 from synth import gen
 from synth.configs import SHAPES, reduced
 
-cases = [("13b", 4096, 16), ("72b", 16384, 32)]
+cases = [("7b", 1024, 16), ("13b", 4096, 16), ("72b", 16384, 32)]
 if len(sys.argv) > 1:
     cases = [c for c in cases if c[0] in sys.argv[1:]] or cases
 for name, ctx, seg in cases:
