@@ -44,6 +44,9 @@ def parse():
                          "cfg4 = configs[3] (13B, scenario S), cfg5 = configs[4] (72B), "
                          "s7b = 7B scenario S")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--real-prefill", action="store_true",
+                    help="synthetic-KV workloads (cfg4/cfg5): real chunked prefill of the whole prefix instead")
+    ap.add_argument("--max-prefill", type=int, default=64, help="rows per prefill chunk (<= 64)")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-attn-long", action="store_true")
     return ap.parse_args()
@@ -93,6 +96,26 @@ def peaks():
         return float(m["hbm_gbs"]), float(m["bf16_tflops"]), "measured"
     except Exception:
         return 6650.0, 1590.0, "fallback"
+
+
+def tflops_sustained():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 1590.0, "fallback"
+
+
+def prefill_flops(shape, n):
+    """Algorithmic FLOPs of a causal prefill of n tokens: the layer
+    GEMMs 2 * params_per_layer * L per token, attention 4 * H * hd per
+    visible key (QK^T and P V, causal: n(n+1)/2 keys), the head for the last
+    token only."""
+    d, hd = shape.d_model, shape.head_dim
+    per_layer = (d * (shape.n_heads + 2 * shape.n_kv_heads) * hd + shape.n_heads * hd * d
+                 + 3 * d * shape.ffn)
+    return (2.0 * per_layer * shape.n_layers * n + 4.0 * shape.n_heads * hd * shape.n_layers * n * (n + 1) / 2
+            + 2.0 * shape.vocab * d)
 
 
 class Clocks:
@@ -356,7 +379,9 @@ def ours(args):
         obj = [F.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.real_prefill:
+        wl["mode"] = "prefill"
     shape = SHAPES[wl["shape"]]
     ranks = wl["ranks"]
     a = len(ranks) - 1
@@ -370,7 +395,7 @@ def ours(args):
     clocks = Clocks(local)   # nvidia-smi needs ~1 s to start sampling
     clocks.start()
     gp = F.Pipeline(shape, n_stages=P, rank=rank, max_ctx=max_ctx, max_live=512, max_seg=wl["max_seg"],
-                    device=local, nccl_id=nccl_id)
+                    device=local, nccl_id=nccl_id, max_prefill=args.max_prefill)
     gp.fs_load_random_weights(SEED)
     prefix = gen.prefix_tokens(SEED, wl["prefix"], shape.vocab)
     inputs, plan_info = plan_schedule(gp, wl, prefix, shape, n_rounds, n_ticks)
@@ -450,6 +475,31 @@ def ours(args):
     if P > 1:
         dist.barrier()
     clk = clocks.stop()
+
+    # chunked prefill of the workload's prefix (f3): CUDA events on the
+    # library stream, max over ranks
+    pre = None
+    if wl["mode"] == "prefill":
+        if P > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pa.record(st)
+        gp.fs_set_prefix(prefix, F.FS_PREFILL)
+        pb.record(st)
+        torch.cuda.synchronize()
+        p_ms = pa.elapsed_time(pb)
+        if P > 1:
+            tt = torch.tensor([p_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            p_ms = float(tt.item())
+        fl = prefill_flops(shape, wl["prefix"])
+        sus, sus_src = tflops_sustained()
+        pre = {"tokens": wl["prefix"], "ms": round(p_ms, 3), "tok_per_s": round(wl["prefix"] / p_ms * 1e3, 1),
+               "tflops": round(fl / p_ms / 1e9, 1), "peak_bf16_sustained": sus, "peak_source": sus_src,
+               "frac": round(fl / p_ms / 1e9 / sus, 4), "chunk_rows": args.max_prefill, "stages": P,
+               "note": "algorithmic FLOPs (2*params*tokens + causal attention + last-token head); the "
+                       "GEMMs carry activations as a bf16 hi/lo pair, so the tensor pipe executes 2x"}
 
     # roofline of the dominant kernel (weight-streaming GEMM)
     hbm, bf16_tf, peak_src = peaks()
@@ -538,6 +588,8 @@ def ours(args):
                               "H2D_SUBMIT, D2H_TICK, ...), not just the live entries"},
         "gpu_launches": int(launches),
     }
+    if pre:
+        rec["prefill"] = pre
     if prof:
         g_ms = prof["gemm_ms"] / max(prof["gemm_launches"], 1)
         g_bytes = prof["gemm_bytes"] / max(prof["gemm_launches"], 1)
@@ -584,11 +636,11 @@ def ours(args):
 
 def ncu_traffic(alg_bytes_per_launch):
     """roofline.traffic: DRAM bytes (read + write) per GEMM launch, from the committed
-    ncu --set full capture of the same build (profiles/r1_ncu_traffic.json: per-class
+    ncu --set full capture of the same build (profiles/r2_ncu_traffic.json: per-class
     DRAM / algorithmic bytes, weighted over a tick) applied to this run's average
     algorithmic bytes per launch; null when the capture is absent."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")) as f:
             ratio = float(json.load(f)["ratio_weighted_per_tick"])
         return round(alg_bytes_per_launch * ratio)
     except Exception:
