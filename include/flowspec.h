@@ -93,6 +93,11 @@ typedef struct fs_config {
                                logits ([max_live][vocab], arena) so that
                                fs_set_acceptance can switch to stochastic
                                acceptance; 0: greedy only */
+  int32_t max_prefill;      /* rows per prefill chunk (P:214 chunked prefill;
+                               <= FS_MAX_SEG; 0 = max_seg).  Chunks run at their
+                               own row width (GEMM N = 2 x 16/32/64) and are
+                               pipelined over the stages: at step t stage p
+                               processes chunk t - p. */
 } fs_config;
 
 typedef struct fs_ctx fs_ctx;
@@ -122,7 +127,10 @@ int fs_load_random_weights(fs_ctx* ctx, uint64_t seed);
 
 #define FS_PREFILL 0  /* chain-mask passes of <= max_seg rows (P:214 chunked prefill) */
 #define FS_SYNTH_KV 1 /* slots [0,n-1) synthetic K/V, last token real (configs 4-5) */
-/* COLLECTIVE.  Build the prefix KV cache and the first sampled token:
+/* COLLECTIVE.  Build the prefix KV cache and the first sampled token
+ * (FS_PREFILL: chunks of cfg.max_prefill rows, causal, pipelined over the
+ * stages — stage p runs chunk t - p at step t, hidden rows move p -> p+1 as
+ * in a verify tick):
  * l_glo = n, *x_new_out = argmax of the last prefix token's logits
  * ("compute the initial KV cache and generate the first sampled token
  * x_new").  Drops any live round.  FS_EINVAL: n < 1, bad token, bad mode;
@@ -298,9 +306,12 @@ int fs_get_profile(fs_ctx* ctx, fs_profile* out);
  * stage), 5 = layer-0 attention, 6 = RMSNorm, 7 = whole stage forward.
  * Launches back to back `iters` times on the library stream and returns the
  * mean CUDA-event time per launch in *us and the algorithmic bytes per
- * launch in *bytes.  Overwrites activations (not the KV context).  Kinds 8-10
+ * launch in *bytes.  Overwrites activations (not the KV context).  kind |
+ * FS_BENCH_WIDE runs them at the prefill-chunk width on the rows of the last
+ * prefill chunk (f3 measurements).  Kinds 8-10
  * (timeline probes, printed to stderr) exist only in a -DFS_DIAG build, which
  * allocates its probe buffers; the product build allocates no device memory. */
+#define FS_BENCH_WIDE 0x100
 int fs_bench_kernel(fs_ctx* ctx, int32_t kind, int32_t iters, double* us, double* bytes);
 
 /* GEMM numerics check (layer `layer` of this rank, which = 0 QKV, 1 O,

@@ -72,6 +72,7 @@ struct LayerW {
   void *wqkv = nullptr, *bqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
   void *g1 = nullptr, *g2 = nullptr;
   GemmOp qkv, o, gu, dn;
+  GemmOp qkv_w, o_w, gu_w, dn_w;   // the other row width (prefill chunks vs tree segments; use_width)
   CUtensorMap tk, tv;   // this layer's K / V cache planes [Hkv * max_ctx][128] (GQA tcgen05 attention)
   CUtensorMap mk, mv;   // the same planes in 64-key boxes (MHA attention, TMA ring)
 };
@@ -102,6 +103,10 @@ struct fs_ctx {
   int P = 1, rank = 0, L0 = 0, L1 = 0, nl = 0;
   bool first = true, last = true, bf = true;
   int esz = 2, npad = 16, n_sms = 148, ancw = 16, max_ids = 65536, gemm_ctas = 2;
+  // row widths: tree segments (npad of max_seg) and prefill chunks (npad of
+  // max_prefill); buffers are carved for the larger, GemmOps exist for both
+  int npad_tick = 16, npad_pre = 16, ctas_tick = 2, ctas_pre = 2;
+  bool wide = false;                // the prefill-chunk width is active
   int att_dbg_ends = 0;
   int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
   int mha_nsplit[3] = {0, 0, 0};   // TMA MHA attention: splits per m-tile count (SM-count sized)
@@ -116,7 +121,7 @@ struct fs_ctx {
   // weights
   std::vector<LayerW> lw;
   void *emb = nullptr, *wh = nullptr, *gf = nullptr;
-  GemmOp head;
+  GemmOp head, head_w;
   // kv / rope
   char* kv = nullptr;
   size_t kv_plane_elems = 0;  // Hkv * max_ctx * hd
@@ -256,6 +261,7 @@ bool cfg_valid(const fs_config* c, std::string* why) {
   }
   if (c->max_live < 32 || c->max_live > FS_MAX_LIVE || c->max_live % 32) return bad("max_live");
   if (c->max_seg < 1 || c->max_seg > FS_MAX_SEG) return bad("max_seg");
+  if (c->max_prefill < 0 || c->max_prefill > FS_MAX_SEG) return bad("max_prefill");
   if (c->max_ctx < c->max_live + 2) return bad("max_ctx");
   if (!c->bf16 && c->max_ctx > 50000) return bad("fp32 path: max_ctx <= 50000 (attention scores in smem)");
   if (c->rms_eps <= 0 || c->rope_theta <= 0) return bad("eps/theta");
@@ -357,21 +363,26 @@ size_t carve(fs_ctx* c, char* base) {
     w.wd = cv.take<char>(wr(d) * ffn * es);
     w.g1 = cv.take<char>((size_t)d * es);
     w.g2 = cv.take<char>((size_t)d * es);
-    plan_gemm(w.qkv, nq, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_QKV");
-    plan_gemm(w.o, d, H * hd, c->n_sms, c->gemm_ctas, "FS_SPLIT_O");
-    plan_gemm(w.gu, 2 * ffn, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_GU");
-    plan_gemm(w.dn, d, ffn, c->n_sms, c->gemm_ctas, "FS_SPLIT_DN");
+    plan_gemm(w.qkv, nq, d, c->n_sms, c->ctas_tick, "FS_SPLIT_QKV");
+    plan_gemm(w.o, d, H * hd, c->n_sms, c->ctas_tick, "FS_SPLIT_O");
+    plan_gemm(w.gu, 2 * ffn, d, c->n_sms, c->ctas_tick, "FS_SPLIT_GU");
+    plan_gemm(w.dn, d, ffn, c->n_sms, c->ctas_tick, "FS_SPLIT_DN");
+    plan_gemm(w.qkv_w, nq, d, c->n_sms, c->ctas_pre);
+    plan_gemm(w.o_w, d, H * hd, c->n_sms, c->ctas_pre);
+    plan_gemm(w.gu_w, 2 * ffn, d, c->n_sms, c->ctas_pre);
+    plan_gemm(w.dn_w, d, ffn, c->n_sms, c->ctas_pre);
   }
   c->emb = c->first ? cv.take<char>((size_t)V * d * es) : nullptr;
   if (c->last) {
     c->wh = cv.take<char>(wr(V) * d * es);
     c->gf = cv.take<char>((size_t)d * es);
-    plan_gemm(c->head, V, d, c->n_sms, c->gemm_ctas, "FS_SPLIT_HEAD");
+    plan_gemm(c->head, V, d, c->n_sms, c->ctas_tick, "FS_SPLIT_HEAD");
+    plan_gemm(c->head_w, V, d, c->n_sms, c->ctas_pre);
   }
   c->kv_plane_elems = (size_t)Hkv * f.max_ctx * hd;
   c->kv = cv.take<char>((size_t)c->nl * 2 * c->kv_plane_elems * es);
   c->rope = cv.take<float2>((size_t)f.max_ctx * (hd / 2));
-  const int np = c->npad;
+  const int np = std::max(c->npad_tick, c->npad_pre);
   c->x = cv.take<float>((size_t)np * d);
   c->hin = cv.take<float>((size_t)np * d);
   // GEMM B operands: 2*np rows (bf16 hi rows, then lo rows)
@@ -394,8 +405,15 @@ size_t carve(fs_ctx* c, char* base) {
     acc(w.o);
     acc(w.gu);
     acc(w.dn);
+    acc(w.qkv_w);
+    acc(w.o_w);
+    acc(w.gu_w);
+    acc(w.dn_w);
   }
-  if (c->last) acc(c->head);
+  if (c->last) {
+    acc(c->head);
+    acc(c->head_w);
+  }
   c->gws_floats = wsf;
   c->gws = c->bf ? cv.take<float>(wsf) : nullptr;
   c->gcnt = cv.take<int>(max_tiles);
@@ -454,8 +472,16 @@ bool setup_ctx(fs_ctx* c, const fs_config* f) {
   c->last = c->rank == c->P - 1;
   c->bf = f->bf16 != 0;
   c->esz = c->bf ? 2 : 4;
-  c->npad = npad_of(f->max_seg);
-  c->gemm_ctas = c->npad <= 16 ? GemmCfg<16>::MIN_CTAS : 1;
+  c->npad_tick = npad_of(f->max_seg);
+  c->npad_pre = npad_of(std::max(f->max_seg, f->max_prefill));
+  // grouped-query heads pack G * npad query rows per kv head; the attention
+  // kernels take at most 256 (two tcgen05 M-tiles): cap the prefill width
+  const int G = f->n_kv_heads > 0 ? f->n_heads / f->n_kv_heads : 1;
+  while (f->bf16 && c->npad_pre > c->npad_tick && G * c->npad_pre > 256) c->npad_pre /= 2;
+  c->ctas_tick = c->npad_tick <= 16 ? GemmCfg<16>::MIN_CTAS : 1;
+  c->ctas_pre = c->npad_pre <= 16 ? GemmCfg<16>::MIN_CTAS : 1;
+  c->npad = c->npad_tick;
+  c->gemm_ctas = c->ctas_tick;
   c->ancw = f->max_live / 32;
   return true;
 }
@@ -487,19 +513,25 @@ char* kv_plane(fs_ctx* c, int local_layer, int which);
 bool build_maps(fs_ctx* c) {
   const fs_config& f = c->cfg;
   const int d = f.d_model, H = f.n_heads, Hkv = f.n_kv_heads, hd = f.head_dim, ffn = f.ffn;
-  const int nq = (H + 2 * Hkv) * hd, np = c->npad;
+  const int nq = (H + 2 * Hkv) * hd;
   bool ok = true;
   for (auto& w : c->lw) {
-    ok &= encode_wmap(&w.qkv.ta, w.wqkv, d, nq);
-    ok &= encode_map(&w.qkv.tb, c->y, d, 2 * np, 64, 2 * np);
-    ok &= encode_wmap(&w.o.ta, w.wo, H * hd, d);
-    ok &= encode_map(&w.o.tb, c->att, H * hd, 2 * np, 64, 2 * np);
-    ok &= encode_wmap(&w.gu.ta, w.wgu, d, 2 * ffn);
-    ok &= encode_map(&w.gu.tb, c->y, d, 2 * np, 64, 2 * np);
-    ok &= encode_wmap(&w.dn.ta, w.wd, ffn, d);
-    ok &= encode_map(&w.dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
-
-    w.qkv.ok = w.o.ok = w.gu.ok = w.dn.ok = ok;
+    for (int wide = 0; wide < 2; wide++) {
+      const int np = wide ? c->npad_pre : c->npad_tick;
+      GemmOp& qkv = wide ? w.qkv_w : w.qkv;
+      GemmOp& o = wide ? w.o_w : w.o;
+      GemmOp& gu = wide ? w.gu_w : w.gu;
+      GemmOp& dn = wide ? w.dn_w : w.dn;
+      ok &= encode_wmap(&qkv.ta, w.wqkv, d, nq);
+      ok &= encode_map(&qkv.tb, c->y, d, 2 * np, 64, 2 * np);
+      ok &= encode_wmap(&o.ta, w.wo, H * hd, d);
+      ok &= encode_map(&o.tb, c->att, H * hd, 2 * np, 64, 2 * np);
+      ok &= encode_wmap(&gu.ta, w.wgu, d, 2 * ffn);
+      ok &= encode_map(&gu.tb, c->y, d, 2 * np, 64, 2 * np);
+      ok &= encode_wmap(&dn.ta, w.wd, ffn, d);
+      ok &= encode_map(&dn.tb, c->act, ffn, 2 * np, 64, 2 * np);
+      qkv.ok = o.ok = gu.ok = dn.ok = ok;
+    }
   }
   for (int l = 0; l < c->nl; l++) {
     LayerW& w = c->lw[l];
@@ -511,11 +543,28 @@ bool build_maps(fs_ctx* c) {
   }
   if (c->last) {
     ok &= encode_wmap(&c->head.ta, c->wh, d, f.vocab);
-    ok &= encode_map(&c->head.tb, c->y, d, 2 * np, 64, 2 * np);
-
-    c->head.ok = ok;
+    ok &= encode_map(&c->head.tb, c->y, d, 2 * c->npad_tick, 64, 2 * c->npad_tick);
+    ok &= encode_wmap(&c->head_w.ta, c->wh, d, f.vocab);
+    ok &= encode_map(&c->head_w.tb, c->y, d, 2 * c->npad_pre, 64, 2 * c->npad_pre);
+    c->head.ok = c->head_w.ok = ok;
   }
   return ok;
+}
+
+// switch the active row width: prefill chunks (wide) or tree segments; the
+// GemmOps of the two widths trade places so every launch site stays as is
+void use_width(fs_ctx* c, bool wide) {
+  if (wide == c->wide) return;
+  for (auto& w : c->lw) {
+    std::swap(w.qkv, w.qkv_w);
+    std::swap(w.o, w.o_w);
+    std::swap(w.gu, w.gu_w);
+    std::swap(w.dn, w.dn_w);
+  }
+  std::swap(c->head, c->head_w);
+  c->wide = wide;
+  c->npad = wide ? c->npad_pre : c->npad_tick;
+  c->gemm_ctas = wide ? c->ctas_pre : c->ctas_tick;
 }
 
 // ---------------------------------------------------------------- profiling
@@ -1008,7 +1057,7 @@ int stage_forward(fs_ctx* c, bool from_hin) {
     embed_kernel<float><<<FS_MAX_SEG, 256, 0, c->st>>>((const float*)c->emb, d, c->d_rows, c->x);
     CK_LAUNCH(c);
   } else if (from_hin) {
-    CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)c->cfg.max_seg * d * 4, cudaMemcpyDeviceToDevice, c->st));
+    CK_CUDA(c, cudaMemcpyAsync(c->x, c->hin, (size_t)c->npad * d * 4, cudaMemcpyDeviceToDevice, c->st));
   }
   for (int l = 0; l < c->nl; l++) {
     int rc = layer_forward(c, l);
@@ -1361,24 +1410,6 @@ static void reset_round(fs_ctx* c) {
   }
 }
 
-// run rows (already in h_rows) through the whole pipeline without overlap:
-// stage p receives from p-1, computes, sends to p+1; the last stage leaves
-// its RowResult in c->res, which is broadcast to all ranks.
-static int run_chunk_through_pipeline(fs_ctx* c) {
-  int rc;
-  const int n = c->h_rows->n_rows;
-  const int d = c->cfg.d_model;
-  if ((rc = upload_rows(c))) return rc;
-  if (c->P > 1 && !c->first && (rc = exchange(c, nullptr, 0, c->x, (size_t)n * d, nullptr, 0))) return rc;
-  if ((rc = stage_forward(c, false))) return rc;
-  if (c->P > 1 && (rc = exchange(c, c->x, c->last ? 0 : (size_t)n * d, nullptr, 0, c->res,
-                                 sizeof(RowResult) * n / 4)))
-    return rc;
-  // h_rows (pinned) is rewritten for the next chunk: the async H2D copy above
-  // must have executed first
-  return sync(c);
-}
-
 int fs_set_prefix(fs_ctx* c, const int32_t* tok, int32_t n, int32_t mode, uint64_t kv_seed,
                   int32_t* x_new_out) {
   int rc;
@@ -1389,7 +1420,6 @@ int fs_set_prefix(fs_ctx* c, const int32_t* tok, int32_t n, int32_t mode, uint64
     if (tok[i] < 0 || tok[i] >= c->cfg.vocab) return fail(c, FS_EINVAL, "bad prefix token");
   if (n + c->cfg.max_live > c->cfg.max_ctx) return fail(c, FS_ECAPACITY, "prefix too long");
   reset_round(c);
-  const int M = c->cfg.max_seg;
   int start = 0;
   if (mode == FS_SYNTH_KV) {
     const fs_config& f = c->cfg;
@@ -1412,28 +1442,56 @@ int fs_set_prefix(fs_ctx* c, const int32_t* tok, int32_t n, int32_t mode, uint64
       }
     start = n - 1;
   }
-  while (start < n) {
-    const int m = std::min(M, n - start);
-    TickRows* r = c->h_rows;
-    r->n_rows = m;
-    r->l_glo = start;
-    r->s_begin = 0;
-    r->n_keys = start + m;
-    for (int i = 0; i < m; i++) {
-      r->token[i] = tok[start + i];
-      r->pos[i] = start + i;
-      r->slot[i] = start + i;
-      r->ctx_lim[i] = start + i + 1;
-      r->sidx[i] = -1;
+  // chunked prefill at the prefill row width, pipelined over the
+  // stages: at step t stage p runs chunk t - p; its input rows arrive from
+  // p-1 at the end of step t-1 (the same exchange as a verify tick)
+  const int M = std::min(std::max(c->cfg.max_seg, c->cfg.max_prefill), c->npad_pre);
+  use_width(c, true);
+  const int n_chunks = (n - start + M - 1) / M;
+  const int p = c->rank, P = c->P, d = c->cfg.d_model;
+  rc = FS_OK;
+  for (int t = 0; t < n_chunks + P - 1; t++) {
+    const int ch = t - p;                       // this stage's chunk this step
+    const bool has = ch >= 0 && ch < n_chunks;
+    const int b0 = start + ch * M;
+    const int m = has ? std::min(M, n - b0) : 0;
+    if (has) {
+      TickRows* r = c->h_rows;
+      r->n_rows = m;
+      r->l_glo = b0;
+      r->s_begin = 0;
+      r->n_keys = b0 + m;
+      for (int i = 0; i < m; i++) {
+        r->token[i] = tok[b0 + i];
+        r->pos[i] = b0 + i;
+        r->slot[i] = b0 + i;
+        r->ctx_lim[i] = b0 + i + 1;
+        r->sidx[i] = -1;
+      }
+      if ((rc = upload_rows(c))) break;
+      if ((rc = stage_forward(c, true))) break;
     }
-    if ((rc = run_chunk_through_pipeline(c))) return rc;
-    // keep the last row's result
-    start += m;
-    if (start >= n) {
-      CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * m, cudaMemcpyDeviceToHost, c->st));
-      if ((rc = sync(c))) return rc;
-      c->x_new = c->h_res[m - 1].am;
+    if (P > 1) {
+      const int chp = t - (p - 1);              // the chunk stage p-1 ran this step
+      const bool recv = p > 0 && chp >= 0 && chp < n_chunks;
+      const int mr = recv ? std::min(M, n - (start + chp * M)) : 0;
+      const int chl = t - (P - 1);              // the last stage's chunk: only the final one's rows matter
+      const bool bc = chl == n_chunks - 1;
+      const int mb = bc ? std::min(M, n - (start + chl * M)) : 0;
+      if ((rc = exchange(c, c->x, (has && !c->last) ? (size_t)m * d : 0, c->hin, (size_t)mr * d, c->res,
+                         (size_t)mb * 2)))
+        break;
     }
+    // h_rows (pinned) is rewritten next step: the async H2D copy must have run
+    if ((rc = sync(c))) break;
+  }
+  use_width(c, false);
+  if (rc) return rc;
+  {
+    const int mlast = n - (start + (n_chunks - 1) * M);
+    CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * mlast, cudaMemcpyDeviceToHost, c->st));
+    if ((rc = sync(c))) return rc;
+    c->x_new = c->h_res[mlast - 1].am;
   }
   c->l_glo = n;
   c->prefixed = true;
@@ -1885,9 +1943,22 @@ int fs_get_profile(fs_ctx* c, fs_profile* out) {
   return FS_OK;
 }
 
+static int bench_kernel_impl(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes);
+
 int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
   int rc;
   if (!check(c, &rc)) return rc;
+  // kind | FS_BENCH_WIDE: the same launches at the prefill-chunk row width, on
+  // the rows of the last prefill chunk
+  const bool wide = (kind & FS_BENCH_WIDE) != 0;
+  use_width(c, wide);
+  rc = bench_kernel_impl(c, kind & ~FS_BENCH_WIDE, iters, us, bytes);
+  use_width(c, false);
+  return rc;
+}
+
+static int bench_kernel_impl(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
+  int rc;
 #ifdef FS_DIAG  // timeline diagnostics (build with -DFS_DIAG): probe buffers allocated here
   if (kind == 9 || kind == 10) {
     // diagnostics: phase probes of attention (9) or O-projection GEMM with its

@@ -33,7 +33,8 @@ class fs_config(C.Structure):
                 ("n_stages", i32), ("rank", i32), ("layers_per_stage", C.POINTER(i32)),
                 ("max_ctx", i32), ("max_live", i32), ("max_seg", i32), ("device", i32),
                 ("arena", C.c_void_p), ("arena_bytes", C.c_size_t), ("stream", C.c_void_p),
-                ("nccl_id", C.POINTER(C.c_uint8)), ("local_group", C.c_void_p), ("sampling", i32)]
+                ("nccl_id", C.POINTER(C.c_uint8)), ("local_group", C.c_void_p), ("sampling", i32),
+                ("max_prefill", i32)]
 
 
 class fs_submit_out(C.Structure):
@@ -126,9 +127,10 @@ def _i32(a):
 
 
 def make_config(shape, n_stages=1, rank=0, max_ctx=4096, max_live=512, max_seg=16, device=0,
-                layers_per_stage=None, sampling=0):
+                layers_per_stage=None, sampling=0, max_prefill=0):
     c = fs_config()
     c.sampling = sampling
+    c.max_prefill = max_prefill
     for k in ("n_layers", "d_model", "n_heads", "n_kv_heads", "head_dim", "ffn", "vocab",
               "qkv_bias", "bf16"):
         setattr(c, k, int(getattr(shape, k)))
@@ -149,13 +151,13 @@ class Pipeline:
 
     def __init__(self, shape, n_stages=1, rank=0, max_ctx=4096, max_live=512, max_seg=16,
                  device=0, layers_per_stage=None, nccl_id=None, stream=None, local_group=None,
-                 sampling=0):
+                 sampling=0, max_prefill=0):
         import torch
         self.torch = torch
         self.L = lib()
         self.shape = shape
         self.cfg = make_config(shape, n_stages, rank, max_ctx, max_live, max_seg, device,
-                               layers_per_stage, sampling)
+                               layers_per_stage, sampling, max_prefill)
         nbytes = self.L.fs_arena_bytes(C.byref(self.cfg))
         if nbytes == 0:
             raise FlowSpecError(FS_EINVAL, "invalid configuration")
@@ -334,7 +336,7 @@ class LocalPipeline:
     COLLECTIVE = ("fs_set_prefix", "fs_verify_step")
 
     def __init__(self, shape, n_stages, max_ctx=4096, max_live=512, max_seg=16, devices=None,
-                 layers_per_stage=None, sampling=0):
+                 layers_per_stage=None, sampling=0, max_prefill=0):
         from concurrent.futures import ThreadPoolExecutor
         self.L = lib()
         self.P = n_stages
@@ -346,7 +348,8 @@ class LocalPipeline:
         devices = devices or [0] * n_stages
         self.stages = [Pipeline(shape, n_stages=n_stages, rank=p, max_ctx=max_ctx, max_live=max_live,
                                 max_seg=max_seg, device=devices[p], layers_per_stage=layers_per_stage,
-                                local_group=g, sampling=sampling) for p in range(n_stages)]
+                                local_group=g, sampling=sampling, max_prefill=max_prefill)
+                       for p in range(n_stages)]
         self.shape = shape
         self.cfg = self.stages[-1].cfg
         self.pool = ThreadPoolExecutor(max_workers=n_stages)

@@ -81,6 +81,10 @@ def test_7b_real_prefill_stream_matches_oracle():
     committed, r, a = [], 0, 4
     while len(committed) + a + 2 <= len(stream) and r < 24 and committed == stream[:len(committed)]:
         c = len(committed)
+        x = gp.state()["x_new"]
+        if x != stream[c]:       # the next root (not yet committed) already parts from the oracle
+            committed.append(x)
+            break
         t = gen.planted_tree(SEED + r, 64, 6, stream[c:c + a + 2], (0, 2, 5, 17, 21), shape.vocab)
         gp.fs_submit_segment(F.FS_NEW_ROUND, t["parent"], t["token"], t["own"], 16)
         while True:
