@@ -388,6 +388,8 @@ def ours(args):
     l_max, n_nodes, depth = wl["l_max"], wl["n_nodes"], wl["depth"]
     W, K = args.warmup, args.steps
     S = wl["scenario"] == "S"
+    if S:   # steady state: the initial tree's segments drained and the pipeline full
+        W = max(W, P + wl["n_nodes"] // wl["l_max"] + 2)
     n_rounds = 0 if S else W + 2 * K
     n_ticks = W + 2 * K if S else 0
     grow = (n_rounds * (a + 1)) if not S else (a + wl["q"] * (n_ticks + 4))

@@ -884,7 +884,14 @@ int launch_attention(fs_ctx* c, int l) {
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
                                            (double)nsplit * Hkv * QR * (hd + 2) * 4 * 2);
       // P as a bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P_BF16)
-      const bool plo = getenv("FS_TC_ATTN_P_BF16") == nullptr;
+      // P format of P.V: bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P=bf16: 38.4 vs
+      // 44.5 us per 72B layer but 0.027 > 2e-2 on the logits); f16 P with bf16 V is not a
+      // valid kind::f16 instruction (illegal instruction on sm_100a: A and B must match)
+      const char* pfe = getenv("FS_TC_ATTN_P");
+      const int pf = getenv("FS_TC_ATTN_P_BF16") ? TCA_P_BF16
+                     : !pfe ? TCA_P_HILO
+                     : !strcmp(pfe, "f16") ? TCA_P_F16
+                     : !strcmp(pfe, "bf16") ? TCA_P_BF16 : TCA_P_HILO;
       auto go = [&](auto kern, int threads, int smem_bytes) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         lc.blockDim = dim3(threads);
@@ -892,11 +899,13 @@ int launch_attention(fs_ctx* c, int l) {
         cudaLaunchKernelEx(&lc, kern, c->lw[l].tk, c->lw[l].tv, ta);
       };
       if (QR == 128) {
-        if (plo) go(attn_gqa_tc_kernel<1, true>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
-        else go(attn_gqa_tc_kernel<1, false>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
+        if (pf == TCA_P_HILO) go(attn_gqa_tc_kernel<1, TCA_P_HILO>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
+        else if (pf == TCA_P_F16) go(attn_gqa_tc_kernel<1, TCA_P_F16>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
+        else go(attn_gqa_tc_kernel<1, TCA_P_BF16>, TcAttnCfg<1>::THREADS, TcAttnCfg<1>::SMEM);
       } else {
-        if (plo) go(attn_gqa_tc_kernel<2, true>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
-        else go(attn_gqa_tc_kernel<2, false>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
+        if (pf == TCA_P_HILO) go(attn_gqa_tc_kernel<2, TCA_P_HILO>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
+        else if (pf == TCA_P_F16) go(attn_gqa_tc_kernel<2, TCA_P_F16>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
+        else go(attn_gqa_tc_kernel<2, TCA_P_BF16>, TcAttnCfg<2>::THREADS, TcAttnCfg<2>::SMEM);
       }
       prof_end(c, api);
       CK_LAUNCH(c);

@@ -92,11 +92,16 @@ FS_DEV uint64_t umma_sdesc_sw128_mn(uint32_t smem_addr, uint32_t lbo, uint32_t s
 }
 FS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int MT2, bool PLO>
+// P formats of the P.V MMA: bf16, bf16 hi + lo pair (two MMAs), fp16 (A f16
+// from TMEM with B = V bf16 in the same kind::f16 instruction)
+constexpr int TCA_P_BF16 = 0, TCA_P_HILO = 1, TCA_P_F16 = 2;
+
+template <int MT2, int PF>
 __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     attn_gqa_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                        TcAttnArgs args) {
   using C = TcAttnCfg<MT2>;
+  constexpr bool PLO = PF == TCA_P_HILO;
   const AttnArgs& a = args.a;
   extern __shared__ uint8_t tsm_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -235,7 +240,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       // Ping-pong over the two M-tiles: after P V of (tile j, M-tile mi) comes
       // Q K^T of (j+1, mi), so one M-tile's softmax overlaps the other's MMAs.
       constexpr uint32_t idesc_qk = umma_idesc_bf16(128, 128);
-      constexpr uint32_t idesc_pv = umma_idesc_bf16(128, 128) | (1u << 16);   // B (V) MN-major
+      constexpr uint32_t idesc_pv = (umma_idesc_bf16(128, 128) | (1u << 16))     // B (V) MN-major
+                                    & (PF == TCA_P_F16 ? ~(7u << 7) : ~0u);          // A (P) f16
       const uint32_t q0 = smem_u32(sQ);
       const uint32_t kv0 = smem_u32(sKV);
       auto stage_of = [&](int j) { return j % C::NST; };
@@ -383,8 +389,14 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
             ls[i & 3] += x0 + x1;
             // P_hi -> columns [0, 32) of the half; P_lo = p - float(P_hi) -> [32, 64)
             // (hi halves unpacked with integer ops, no second rounding)
-            const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
-            const uint32_t u = *reinterpret_cast<const uint32_t*>(&hb);
+            uint32_t u;
+            if constexpr (PF == TCA_P_F16) {
+              const __half2 hf = __floats2half2_rn(x0, x1);
+              u = *reinterpret_cast<const uint32_t*>(&hf);
+            } else {
+              const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+              u = *reinterpret_cast<const uint32_t*>(&hb);
+            }
             pk[i] = u;
             if constexpr (PLO)
               pl[i] = pack_bf16(x0 - __uint_as_float(u << 16), x1 - __uint_as_float(u & 0xFFFF0000u));
