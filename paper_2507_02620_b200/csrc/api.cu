@@ -884,9 +884,10 @@ int launch_attention(fs_ctx* c, int l) {
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
                                            (double)nsplit * Hkv * QR * (hd + 2) * 4 * 2);
       // P as a bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P_BF16)
-      // P format of P.V: bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P=bf16: 38.4 vs
-      // 44.5 us per 72B layer but 0.027 > 2e-2 on the logits); f16 P with bf16 V is not a
-      // valid kind::f16 instruction (illegal instruction on sm_100a: A and B must match)
+      // P format of P.V: bf16 hi/lo pair (default), plain bf16 (FS_TC_ATTN_P=bf16: 38.4 vs
+      // 44.5 us per 72B layer but 0.027 > 2e-2 on the logits) or fp16 with V converted to
+      // fp16 in shared memory (FS_TC_ATTN_P=f16; f16 P with bf16 V is not a valid
+      // kind::f16 instruction: A and B formats must match)
       const char* pfe = getenv("FS_TC_ATTN_P");
       const int pf = getenv("FS_TC_ATTN_P_BF16") ? TCA_P_BF16
                      : !pfe ? TCA_P_HILO

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   uint64_t* p_full = s_full + 2;         // [MT2]
   uint64_t* pv_done = p_full + 2;        // [MT2]: P V of the step complete (S/P columns free)
   uint64_t* o_full = pv_done + 2;        // [MT2]: the M-tile's last P V complete
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* v_ready = o_full + 2;        // [NST] (f16 P): the stage's V converted to fp16
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(v_ready + 2);
   int* sCtxMin = reinterpret_cast<int*>(tmem_holder + 1);
   uint32_t* sAnc = reinterpret_cast<uint32_t*>(smem + C::Q_BYTES + C::NST * C::STAGE_BYTES + 256);
 
@@ -160,6 +161,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     mbar_init(&o_full[0], 1);
     mbar_init(&o_full[1], 1);
+    for (int st = 0; st < C::NST; st++) mbar_init(&v_ready[st], 62);
     fence_barrier_init();
   }
   const int n_rows = rows->n_rows;
@@ -214,6 +216,32 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   __syncthreads();
   TCA_PROBE(1);
 
+  if constexpr (PF == TCA_P_F16) {
+    if (warp <= 1 && lane > 0) {
+      // ---------------- V bf16 -> fp16 in place (62 lanes of the producer and MMA
+      // warps): element-wise, so the SW128 layout the MMA reads is unchanged;
+      // exact for |v| in [2^-14, 65504] (fp16 normal range; smaller values keep
+      // their fp16-subnormal part, an absolute error below 2^-25)
+      const int cid = warp * 31 + (lane - 1);
+      for (int j = 0; j < T; j++) {
+        const int st = j % C::NST;
+        mbar_wait(&full[st], (uint32_t)((j / C::NST) & 1));
+        uint4* v = reinterpret_cast<uint4*>(sKV + st * C::STAGE_BYTES + 2 * TCA_BOX);
+        for (int i = cid; i < 2 * TCA_BOX / 16; i += 62) {
+          uint4 x = v[i];
+          uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const __half2 h = __floats2half2_rn(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xFFFF0000u));
+            w[k] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+          v[i] = x;
+        }
+        fence_proxy_async_smem();   // the MMA reads V through the async proxy
+        mbar_arrive(&v_ready[st]);
+      }
+    }
+  }
   if (warp == 0) {
     if (lane == 0) {   // ---------------- TMA producer: K + V tiles
       const uint64_t pol = l2_evict_first_policy();
@@ -241,7 +269,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       // Q K^T of (j+1, mi), so one M-tile's softmax overlaps the other's MMAs.
       constexpr uint32_t idesc_qk = umma_idesc_bf16(128, 128);
       constexpr uint32_t idesc_pv = (umma_idesc_bf16(128, 128) | (1u << 16))     // B (V) MN-major
-                                    & (PF == TCA_P_F16 ? ~(7u << 7) : ~0u);          // A (P) f16
+                                    & (PF == TCA_P_F16 ? ~((7u << 7) | (7u << 10)) : ~0u);   // A, B f16
       const uint32_t q0 = smem_u32(sQ);
       const uint32_t kv0 = smem_u32(sKV);
       auto stage_of = [&](int j) { return j % C::NST; };
@@ -262,6 +290,8 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       };
       auto issue_pv = [&](int j, int mi) {
         mbar_wait(&p_full[mi], (uint32_t)(j & 1));   // P of this tile written (and O rescaled)
+        if constexpr (PF == TCA_P_F16)
+          if (mi == 0) mbar_wait(&v_ready[stage_of(j)], (uint32_t)((j / C::NST) & 1));
         tc_fence_after();
         const uint32_t v0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES) + 2 * TCA_BOX;
         const uint32_t tS = tmem + (uint32_t)(mi * 256), tO = tS + 128;
