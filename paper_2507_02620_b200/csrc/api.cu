@@ -144,6 +144,7 @@ struct fs_ctx {
   cudaGraphExec_t fwd_exec = nullptr;
   uint64_t fwd_kernels = 0;
   float* fwd_logits = nullptr;
+  int fwd_mha_tma = -1;   // the MHA kernel choice baked into the graph (by context length)
   bool use_graph = true;
   int att_chunk_cap = 0;
   size_t gws_floats = 0;
@@ -750,7 +751,13 @@ int launch_attention(fs_ctx* c, int l) {
     const int G = H / Hkv, QR = G * np, MT = QR / 16;
     const int KS = MT >= 4 ? 1 : 4 / MT;
     const int n_keys = c->h_rows->n_keys;
-    if (MT <= 2 && hd == ATT_HD && !getenv("FS_MHA_CP_ASYNC")) {
+    // MHA: short contexts run the cluster kernel (split merge through DSMEM, no
+    // second kernel: 7B 1K context 2.72 vs 2.86 ms per tick), long contexts the
+    // TMA ring + combine (13B 4K context 16.4 vs 23.0 us per layer)
+    const bool mha_tma = getenv("FS_MHA_CP_ASYNC") ? false
+                         : getenv("FS_MHA_TMA") ? true
+                         : n_keys > MHA_TMA_MIN_KEYS;
+    if (MT <= 2 && hd == ATT_HD && mha_tma) {
       // MHA path: TMA-staged K/V ring, splits sized to fill every SM slot,
       // partials merged by attn_combine_kernel (programmatic launch)
       const size_t smem = mha_tma_smem(np, c->ancw);
@@ -1081,7 +1088,8 @@ int stage_forward(fs_ctx* c, bool from_hin) {
 // d_rows, so one graph serves every tick); direct launches when profiling
 int tick_forward(fs_ctx* c) {
   if (!c->use_graph || c->prof) return stage_forward(c, true);
-  if (c->fwd_exec && c->fwd_logits != head_logits(c)) {
+  const int want_tma = c->h_rows->n_keys > MHA_TMA_MIN_KEYS ? 1 : 0;
+  if (c->fwd_exec && (c->fwd_logits != head_logits(c) || c->fwd_mha_tma != want_tma)) {
     cudaGraphExecDestroy(c->fwd_exec);
     c->fwd_exec = nullptr;
   }
@@ -1098,6 +1106,7 @@ int tick_forward(fs_ctx* c) {
     c->fwd_kernels = c->launches - l0;
     c->launches = l0;
     c->fwd_logits = head_logits(c);
+    c->fwd_mha_tma = want_tma;
   }
   CK_CUDA(c, cudaGraphLaunch(c->fwd_exec, c->st));
   c->launches += c->fwd_kernels;

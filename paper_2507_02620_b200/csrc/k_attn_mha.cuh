@@ -29,6 +29,7 @@ constexpr int MHA_NST = FS_MHA_NST;                 // ring depth (sub-chunks)
 constexpr int MHA_BOX = ATT_SUB * 128;             // one [64 keys][64 dims] bf16 box = 8 KB
 constexpr int MHA_STAGE = 4 * MHA_BOX;             // K (2 boxes) | V (2 boxes) = 32 KB
 constexpr int MHA_THREADS = 160;                   // 4 consumer warps + 1 TMA warp
+constexpr int MHA_TMA_MIN_KEYS = 2048;             // shorter contexts: the cluster kernel
 // dynamic smem: ring | Q [32][LD] | anc [npad][ancw] | barriers
 __host__ __device__ constexpr size_t mha_tma_smem(int npad, int ancw) {
   return 1024 + (size_t)MHA_NST * MHA_STAGE + (size_t)ATT_MAXQR * ATT_LD * 2 + (size_t)npad * ancw * 4 + 256;

@@ -214,3 +214,14 @@ def test_tiny_capacity_tree_max_live():
                       l_max=16, tol=1e-4)
     assert st.max_abs <= 1e-4
     print(f"tiny capacity: max|dlogit| {st.max_abs:.3e} rows {st.rows} decisions {st.decisions}")
+
+
+@pytest.mark.parametrize("name", ["small", "smallq"])
+def test_mha_tma_kernel_short_context(name, monkeypatch):
+    """The TMA-ring MHA kernel (k_attn_mha.cuh) normally runs only above 2048
+    keys; forced here on short contexts (ragged last sub-chunk, empty splits)."""
+    monkeypatch.setenv("FS_MHA_TMA", "1")
+    F, shape, gp, op, xo, xg = _pair(name, max_ctx=1024, prefix_len=40)
+    st = run_lockstep(gp, op, planted_trees(shape, 30, 5, (0, 2, 5, 17, 21), SEED), n_rounds=2,
+                      l_max=16, tol=2e-2)
+    assert st.max_abs <= 2e-2
