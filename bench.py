@@ -187,7 +187,7 @@ H2D_PRUNE = 4 * (4 + 512)
 def run_round(gp, tree, l_max, tokens_out=None):
     """One SD round: submit, ticks, accept, prune until the round exits."""
     from paper_2507_02620_b200 import flowspec as F
-    gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], l_max)
+    gp.fs_submit_segment(F.FS_NEW_ROUND | F.FS_SUBMIT_ASYNC, tree["parent"], tree["token"], tree["own"], l_max)
     committed = 0
     ticks = 0
     while True:
@@ -203,6 +203,20 @@ def run_round(gp, tree, l_max, tokens_out=None):
         PRUNES[0] += 1
         if not d.cont:
             return committed, ticks
+
+
+class Batches:
+    """The appended batches of a scenario-S run, generated before the timed
+    region (the draft side is out of scope; its host work is not the path's)."""
+
+    def __init__(self, exp, n):
+        self.items = [exp.next_batch() for _ in range(n)]
+        self.i = 0
+
+    def next_batch(self):
+        b = self.items[self.i]
+        self.i += 1
+        return b
 
 
 class SteadyRound:
@@ -231,7 +245,7 @@ class SteadyRound:
                 return c
         if append:
             par, tok, own = self.exp.next_batch()
-            gp.fs_submit_segment(self.F.FS_APPEND, par, tok, own, self.l_max)
+            gp.fs_submit_segment(self.F.FS_APPEND | self.F.FS_SUBMIT_ASYNC, par, tok, own, self.l_max)
         return c
 
     def end(self, tokens_out=None):
@@ -406,8 +420,8 @@ def ours(args):
 
     if S:
         t0_tree, plan = inputs
-        sr = SteadyRound(gp, t0_tree, gen.SteadyExpansion(SEED + 1, t0_tree, plan, wl["q"], 16, shape.vocab),
-                         l_max)
+        sr = SteadyRound(gp, t0_tree, Batches(gen.SteadyExpansion(SEED + 1, t0_tree, plan, wl["q"], 16,
+                                                                  shape.vocab), n_ticks), l_max)
 
         def step(i):
             return sr.tick(), 1

@@ -155,6 +155,12 @@ int fs_set_prefix(fs_ctx* ctx, const int32_t* tok, int32_t n, int32_t mode,
  * optional top-L_top of them, own segments: S_mer = S_pr || S_app).
  * out->merged[i] = node id of T_new node i (existing or new). */
 #define FS_MERGE 8
+/* OR-ed into NEW_ROUND / APPEND flags (L_top 0): do not wait for the device.
+ * The segments are enqueued from n alone; validation still runs on the device
+ * and a rejected batch poisons the context at the next fs_verify_step
+ * (FS_EPOISONED afterwards).  out (optional) then gets n, s_base and the
+ * segment bounds but no order. */
+#define FS_SUBMIT_ASYNC 16
 typedef struct fs_submit_out {
   int32_t n;                     /* nodes added (after optional top-L) */
   int32_t s_base;                /* S index of the first added node */

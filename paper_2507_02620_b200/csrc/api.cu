@@ -114,6 +114,7 @@ struct fs_ctx {
   ncclComm_t comm = nullptr;
   fs_local_group* lg = nullptr;           // single-process stage transport (else NCCL)
   cudaEvent_t ev_ready = nullptr;         // local transport: this rank's outgoing data ready
+  cudaEvent_t ev_sub = nullptr;           // the last submit's host -> device copy (async submits)
   cudaEvent_t ev_done[FS_MAX_STAGES] = {}; // local transport: copy from rank q finished
   // arena
   char* base = nullptr;
@@ -1523,7 +1524,9 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   int rc;
   if (!check(c, &rc)) return rc;
   if (!c->prefixed) return fail(c, FS_ESTATE, "no prefix");
-  const int32_t kind = flags & ~FS_ORDER_BFS;
+  const int32_t kind = flags & ~(FS_ORDER_BFS | FS_SUBMIT_ASYNC);
+  const bool async = (flags & FS_SUBMIT_ASYNC) != 0;
+  if (async && (kind == FS_MERGE || (L_top > 0 && L_top < n))) return fail(c, FS_EINVAL, "async submit: no merge / top-L");
   if (kind != FS_NEW_ROUND && kind != FS_APPEND && kind != FS_MERGE) return fail(c, FS_EINVAL, "bad flags");
   const bool merge = kind == FS_MERGE;
   if (merge && parent && n >= 1) {   // T_new: parent indices within T_new, node 0 the root
@@ -1545,6 +1548,8 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   if (c->samp_mode && base + n > c->q_rows) return fail(c, FS_ECAPACITY, "node id beyond the draft distributions (q_rows)");
   if ((nr ? 0 : c->n_live) + n_keep > c->cfg.max_live) return fail(c, FS_ECAPACITY, "max_live");
   if (c->l_glo + (nr ? 0 : c->n_live) + n_keep > c->cfg.max_ctx) return fail(c, FS_ECAPACITY, "max_ctx");
+  // the pinned staging struct is reused: the previous (asynchronous) copy must have run
+  if (c->ev_sub) CK_CUDA(c, cudaEventSynchronize(c->ev_sub));
   SubmitIn* s = c->h_sub;
   s->n = n;
   s->flags = flags;
@@ -1562,6 +1567,33 @@ int fs_submit_segment(fs_ctx* c, int32_t flags, const int32_t* parent, const int
   submit_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, merge ? c->d_sub2 : c->d_sub, c->d_rec,
                                                nr ? 0 : c->n_live, c->cfg.vocab, c->x_new, nr ? 1 : 0);
   CK_LAUNCH(c);
+  if (async) {
+    if (!c->ev_sub) CK_CUDA(c, cudaEventCreateWithFlags(&c->ev_sub, cudaEventDisableTiming));
+    CK_CUDA(c, cudaEventRecord(c->ev_sub, c->st));
+    const int s_base = nr ? 0 : c->n_live;
+    if (out) {
+      out->n = n;
+      out->s_base = s_base;
+      out->seg_id0 = c->seg_counter;
+    }
+    int k = 0;
+    for (int b = 0; b < n; b += L_max, k++) {
+      Seg sg;
+      sg.id = c->seg_counter++;
+      sg.b = s_base + b;
+      sg.e = s_base + std::min(b + L_max, n);
+      c->queue.push_back(sg);
+      if (out) out->seg_begin[k] = sg.b;
+    }
+    if (out) {
+      out->n_segs = k;
+      out->seg_begin[k] = s_base + n;
+    }
+    c->n_live = s_base + n;
+    c->next_id = base + n;
+    c->live = 1;
+    return FS_OK;
+  }
   CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, offsetof(TreeRecord, acc_s), cudaMemcpyDeviceToHost, c->st));
   if ((rc = sync(c))) return rc;
   const TreeRecord* r = c->h_rec;
@@ -1695,6 +1727,10 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
       c->plan_ready = acc;
     }
     if ((rc = sync(c))) return rc;
+    if (c->h_rec->sub_err) {
+      c->poisoned = true;
+      return fail(c, FS_EINVAL, "an asynchronous submit was rejected by validation");
+    }
     if (out)
       for (int m = 0; m < n; m++) {
         out->node[m] = c->h_rec->tick_node[m];
@@ -2315,6 +2351,7 @@ void fs_destroy(fs_ctx* c) {
     if (c->lg->member[c->rank] == c) c->lg->member[c->rank] = nullptr;
   }
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->ev_sub) cudaEventDestroy(c->ev_sub);
   for (int q = 0; q < FS_MAX_STAGES; q++)
     if (c->ev_done[q]) cudaEventDestroy(c->ev_done[q]);
   if (c->fwd_exec) cudaGraphExecDestroy(c->fwd_exec);

@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
   }
   __syncthreads();
   if (s_err) {
-    if (i == 0) rec->err = s_err;
+    if (i == 0) {
+      rec->err = s_err;
+      if (in->flags & FS_SUBMIT_ASYNC) rec->sub_err = s_err;
+    }
     return;
   }
   // Eq. 1: cu = own * cu(parent), fp32 RN, folded root -> node;
@@ -163,7 +166,10 @@ __global__ void __launch_bounds__(TREE_THREADS) submit_kernel(TreeDev t, const S
   if (i == 0) s_flag = (n_live + n_keep > t.max_live) ? -4 : 0;
   __syncthreads();
   if (s_flag) {
-    if (i == 0) rec->err = s_flag;
+    if (i == 0) {
+      rec->err = s_flag;
+      if (in->flags & FS_SUBMIT_ASYNC) rec->sub_err = s_flag;
+    }
     return;
   }
   const bool keep = i < n && rank < n_keep;

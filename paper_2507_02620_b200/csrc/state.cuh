@@ -54,6 +54,7 @@ struct TreeRecord {
   int32_t progress, n_acc, x_new, n_new_s, n_new_id, cont, n_flagged;
   int32_t n_pr;             // |I_pr| (prune)
   int32_t n_batch;          // merge: nodes of T_new whose path is new (ids base .. base+n_batch-1)
+  int32_t sub_err;          // sticky: an asynchronous submit's validation error (read by the next verify)
   int32_t order[MAXLIVE];   // submit: batch node ids in S order
   int32_t merged[MAXLIVE];  // merge: node id of every T_new node (existing or new)
   int32_t acc_s[MAXLIVE];   // accept: S indices of S_acc

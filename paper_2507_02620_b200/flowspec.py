@@ -20,6 +20,7 @@ FS_PREFILL, FS_SYNTH_KV = 0, 1
 FS_NEW_ROUND, FS_APPEND = 1, 2
 FS_ORDER_BFS = 4   # OR into submit flags: breadth-first order (w/o-SBD ablation)
 FS_MERGE = 8       # submit kind: merge a tree rooted at the current root (f4 expansion)
+FS_SUBMIT_ASYNC = 16   # OR into NEW_ROUND / APPEND: do not wait (errors poison at the next verify)
 FS_ACCEPT_GREEDY, FS_ACCEPT_STOCHASTIC = 0, 1
 FS_Q_STATE, FS_Q_NODE, FS_Q_TOKEN, FS_Q_PARENT, FS_Q_POS, FS_Q_ANC, FS_Q_CU, FS_Q_RETAIN = range(8)
 
@@ -217,7 +218,7 @@ class Pipeline:
                                            len(p), l_top, l_max, C.byref(out)), "fs_submit_segment")
         bounds = [(out.seg_begin[k], out.seg_begin[k + 1]) for k in range(out.n_segs)]
         r = dict(order=list(out.order[:out.n]), s_base=out.s_base, bounds=bounds, seg_id0=out.seg_id0)
-        if (flags & ~FS_ORDER_BFS) == FS_MERGE:
+        if (flags & ~(FS_ORDER_BFS | FS_SUBMIT_ASYNC)) == FS_MERGE:
             r["merged"] = list(out.merged[:len(p)])
         return r
 

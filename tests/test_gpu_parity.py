@@ -225,3 +225,36 @@ def test_mha_tma_kernel_short_context(name, monkeypatch):
     st = run_lockstep(gp, op, planted_trees(shape, 30, 5, (0, 2, 5, 17, 21), SEED), n_rounds=2,
                       l_max=16, tol=2e-2)
     assert st.max_abs <= 2e-2
+
+
+def test_async_submit_lockstep_and_deferred_error():
+    """FS_SUBMIT_ASYNC: the same rounds without waiting for the device at
+    submit (bench.py's timed path); a batch the device rejects poisons the
+    context at the next verify step instead of corrupting it."""
+    F, shape, gp, op, xo, xg = _pair("small", max_ctx=1024, prefix_len=40)
+    trees = planted_trees(shape, 30, 5, (0, 2, 5, 17, 21), SEED)
+    for r in range(2):
+        t = trees(r, op)
+        so = op.submit(True, t["parent"], t["token"], t["own"], l_max=16)
+        sg = gp.fs_submit_segment(F.FS_NEW_ROUND | F.FS_SUBMIT_ASYNC, t["parent"], t["token"], t["own"], 16)
+        assert sg["bounds"] == [tuple(b) for b in so["bounds"]]
+        compare_tree(gp, op, gp.cfg.max_live // 32, f"async submit r{r}")
+        while True:
+            og, oo = gp.fs_verify_step(), op.verify_step()
+            assert og["node"] == oo["node"]
+            dg, do = gp.decision_dict(gp.fs_accept()), op.accept()
+            if not do["progress"]:
+                continue
+            want = dict(acc_ids=do["acc_ids"], x_new=do["x_new"], n_new_id=do["n_new_id"], cont=do["cont"])
+            gp.fs_prune_and_compact(want)
+            op.prune(want)
+            if not do["cont"]:
+                break
+    # duplicate sibling token: rejected on the device, surfaces at the next verify
+    x = gp.state()["x_new"]
+    gp.fs_submit_segment(F.FS_NEW_ROUND | F.FS_SUBMIT_ASYNC, [-1, 0, 0], [x, 5, 5], [1.0, 0.5, 0.4], 16)
+    with pytest.raises(F.FlowSpecError):
+        gp.fs_verify_step()
+    with pytest.raises(F.FlowSpecError) as e:
+        gp.fs_accept()
+    assert e.value.code == F.FS_EPOISONED
