@@ -217,7 +217,8 @@ class Pipeline:
         self._chk(self.L.fs_submit_segment(self.h, flags, pp, pt, o.ctypes.data_as(C.POINTER(C.c_float)),
                                            len(p), l_top, l_max, C.byref(out)), "fs_submit_segment")
         bounds = [(out.seg_begin[k], out.seg_begin[k + 1]) for k in range(out.n_segs)]
-        r = dict(order=list(out.order[:out.n]), s_base=out.s_base, bounds=bounds, seg_id0=out.seg_id0)
+        order = [] if flags & FS_SUBMIT_ASYNC else list(out.order[:out.n])   # async: not read back
+        r = dict(order=order, s_base=out.s_base, bounds=bounds, seg_id0=out.seg_id0)
         if (flags & ~(FS_ORDER_BFS | FS_SUBMIT_ASYNC)) == FS_MERGE:
             r["merged"] = list(out.merged[:len(p)])
         return r
