@@ -63,7 +63,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     shape = SHAPES[args.shape]
-    ranks = bench.workload(P)["ranks"]
+    ranks = bench.WORKLOADS["cfg2" if P == 1 else "cfg3"]["ranks"]
     a = len(ranks) - 1
     R = args.warmup + args.rounds
     per_round = a + 1 + args.q * args.batches
