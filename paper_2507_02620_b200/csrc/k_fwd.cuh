@@ -192,6 +192,22 @@ FS_DEV void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+FS_DEV void mma_f16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                          uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two bf16 (one 32-bit register) -> two fp16, exact in fp16's normal range
+FS_DEV uint32_t bf16x2_to_f16x2(uint32_t v) {
+  const __half2 h = __floats2half2_rn(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+#ifndef FS_MHA_P16
+#define FS_MHA_P16 1
+#endif
 FS_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -624,6 +640,28 @@ FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, con
     w.oacc[j][2] *= corr[1];
     w.oacc[j][3] *= corr[1];
   }
+#if FS_MHA_P16
+  // O += P V in fp16: P rounded to fp16 (R18 allows rounding P for P.V; 2^-12
+  // relative, finer than bf16) and the V fragments converted bf16 -> fp16 in
+  // registers (exact in fp16's normal range): one MMA per fragment instead of
+  // the hi/lo pair's two
+#pragma unroll
+  for (int kk = 0; kk < KPW / 16; kk++) {
+    uint32_t pf[4];
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      const int jt = 2 * kk + (f >> 1), e0 = (f & 1) * 2;
+      const __half2 h = __floats2half2_rn(sacc[jt][e0], sacc[jt][e0 + 1]);
+      pf[f] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      uint32_t b0, b1;
+      ldsm_x2_t(b0, b1, kv_chunk<SW, ATT_SUB>(sV, kb + kk * 16 + (lane & 15), j * 8));
+      mma_f16_16816(w.oacc[j], pf[0], pf[1], pf[2], pf[3], bf16x2_to_f16x2(b0), bf16x2_to_f16x2(b1));
+    }
+  }
+#else
   // O += P V with P as a bf16 hi + lo pair (R18: fp32 softmax/accumulation)
 #pragma unroll
   for (int kk = 0; kk < KPW / 16; kk++) {
@@ -644,6 +682,7 @@ FS_DEV void mha_subchunk(MhaWarp<KPW>& w, const AttnArgs& a, const bf16* sK, con
       mma_bf16_16816(w.oacc[j], pl[0], pl[1], pl[2], pl[3], b0, b1);
     }
   }
+#endif
 }
 
 // merge the KS key-warps of each m-tile into the CTA partial sPart [QR][HD] +
