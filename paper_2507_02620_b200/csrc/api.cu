@@ -1829,7 +1829,17 @@ int fs_prune_and_compact(fs_ctx* c, const fs_accept_out* dcs) {
   if (nc > 0) {
     const int chunks = c->cfg.head_dim * c->esz / 16;
     const int planes = c->nl * 2 * c->cfg.n_kv_heads;
-    if (chunks == 16)
+    const size_t sm = (size_t)nc * chunks * 16;
+    if (chunks == 16 && !getenv("FS_KV_COMPACT_SERIAL")) {
+      // one round trip per plane through shared memory (<= 512 rows x 256 B)
+      static std::atomic<uint64_t> kattr{0};
+      once_per_device(kattr, c, [] {
+        cudaFuncSetAttribute(kv_compact_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             FS_MAX_LIVE * 16 * 16);
+      });
+      kv_compact_smem_kernel<16><<<planes, 256, sm, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc,
+                                                             c->l_glo);
+    } else if (chunks == 16)
       kv_compact_kernel<16><<<planes, 16, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);
     else if (chunks == 4)
       kv_compact_kernel<4><<<planes, 4, 0, c->st>>>((uint4*)c->kv, c->cfg.max_ctx, c->tree.rank, nc, c->l_glo);

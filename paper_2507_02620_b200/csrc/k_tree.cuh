@@ -606,6 +606,31 @@ __global__ void kv_compact_kernel(uint4* kv, int64_t plane_rows, const int32_t* 
   }
 }
 
+// The same gather with one round trip per plane: a 256-thread CTA loads every
+// moving chunk of its plane into shared memory (all loads in flight, coalesced
+// along the row), then stores them at their ranks.  Reads complete before any
+// write, so overlapping source / destination rows are safe.  Dynamic shared
+// memory: n_cached * CHUNKS * 16 bytes (<= max_live rows).
+template <int CHUNKS>
+__global__ void __launch_bounds__(256) kv_compact_smem_kernel(uint4* kv, int64_t plane_rows,
+                                                              const int32_t* rank, int32_t n_cached,
+                                                              int32_t l_glo) {
+  extern __shared__ uint4 kv_stage[];
+  uint4* base = kv + (size_t)blockIdx.x * plane_rows * CHUNKS;
+  const int n = n_cached * CHUNKS;
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int s = idx / CHUNKS;
+    const int r = rank[s];
+    if (r >= 0 && r != s) kv_stage[idx] = base[(size_t)(l_glo + s) * CHUNKS + idx % CHUNKS];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int s = idx / CHUNKS;
+    const int r = rank[s];
+    if (r >= 0 && r != s) base[(size_t)(l_glo + r) * CHUNKS + idx % CHUNKS] = kv_stage[idx];
+  }
+}
+
 // In-flight hidden rows of a segment (S range [s_b, s_b+n_rows)) keep the
 // rows whose S index is retained (I_local); order preserved.
 __global__ void rows_compact_kernel(float4* h, int32_t d4, const int32_t* rank, int32_t s_b,
