@@ -1,20 +1,16 @@
 # Round-2 multi-GPU evidence (one box, 4 GPUs): NCCL pipeline lockstep tests,
-# then the default bench workload (configs[1] rounds, strong scaling) and the
-# 7B scenario-S workload at N = 1, 2, 4 (one rank per GPU over NCCL).
+# then the default bench workload (configs[1] rounds, strong scaling), the 7B
+# and 13B scenario-S workloads and configs[4] (72B) at N = 1, 2, 4 (one rank
+# per GPU over NCCL), and the f1 ablation at P = 4.
 set -x
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_multi.py -q -rs > gpurun_out/sc2_multi.log 2>&1
-python bench.py --no-cpu-baseline --no-attn-long > gpurun_out/sc2_cfg2_n1.json 2> gpurun_out/sc2_cfg2_n1.err
-for N in 2 4; do
-  python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2951$N \
-    bench.py --gpus $N > gpurun_out/sc2_cfg2_n$N.json 2> gpurun_out/sc2_cfg2_n$N.err
+python -m pytest tests/test_gpu_multi.py -q -rs > gpurun_out/sc3_multi.log 2>&1
+for W in cfg2 s7b cfg4 cfg5; do
+  for N in 1 2 4; do
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29$N$((RANDOM % 90 + 10)) \
+      bench.py --gpus $N --workload $W --no-cpu-baseline --no-attn-long > gpurun_out/sc3_${W}_n$N.json 2> gpurun_out/sc3_${W}_n$N.err
+  done
 done
-for N in 1 2 4; do
-  python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2961$N \
-    bench.py --gpus $N --workload s7b --no-cpu-baseline --no-attn-long > gpurun_out/sc2_s7b_n$N.json 2> gpurun_out/sc2_s7b_n$N.err
-done
-for N in 2 4; do
-  python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2971$N \
-    bench.py --gpus $N --workload cfg4 --no-cpu-baseline --no-attn-long > gpurun_out/sc2_cfg4_n$N.json 2> gpurun_out/sc2_cfg4_n$N.err
-done
-tail -3 gpurun_out/sc2_multi.log
+python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29471 \
+  tools/ablation.py > gpurun_out/sc3_ablation_p4.json 2> gpurun_out/sc3_ablation_p4.err
+tail -3 gpurun_out/sc3_multi.log
