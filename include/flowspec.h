@@ -314,7 +314,9 @@ int fs_get_profile(fs_ctx* ctx, fs_profile* out);
  * mean CUDA-event time per launch in *us and the algorithmic bytes per
  * launch in *bytes.  Overwrites activations (not the KV context).  kind |
  * FS_BENCH_WIDE runs them at the prefill-chunk width on the rows of the last
- * prefill chunk (f3 measurements).  Kinds 8-10
+ * prefill chunk (f3 measurements).  11 = the stochastic accept walk on the
+ * live tree (f2; *bytes = the bytes read per walked node), 12 = the merge
+ * kernel on the last FS_MERGE batch (f4).  Kinds 8-10
  * (timeline probes, printed to stderr) exist only in a -DFS_DIAG build, which
  * allocates its probe buffers; the product build allocates no device memory. */
 #define FS_BENCH_WIDE 0x100

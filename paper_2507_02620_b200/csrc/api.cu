@@ -2024,6 +2024,48 @@ int fs_bench_kernel(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* 
 
 static int bench_kernel_impl(fs_ctx* c, int32_t kind, int32_t iters, double* us, double* bytes) {
   int rc;
+  if (kind == 11 || kind == 12) {
+    // 11: the stochastic accept walk (f2) on the current tree; 12: the merge
+    // kernel (f4) on the T_new of the last FS_MERGE submit.  Back-to-back
+    // launches; they only rewrite the decision / merge scratch.
+    if (!c->live || iters < 1 || !us || !bytes) return fail(c, FS_EINVAL, "bad bench request");
+    if (kind == 11 && !(c->samp_mode && c->lstore)) return fail(c, FS_ESTATE, "stochastic mode on the last stage");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    SampleArgs sa;
+    if (kind == 11) {
+      sa.t = c->tree;
+      sa.lstore = c->lstore;
+      sa.q = c->q_dev;
+      sa.q_rows = c->q_rows;
+      sa.V = c->cfg.vocab;
+      sa.n_live = c->n_live;
+      sa.inv_temp = c->inv_temp;
+      sa.seed = c->samp_seed;
+      sa.flag = 1e-6;
+      sa.r = c->samp_r;
+      sa.qs = c->samp_q;
+      sa.dec = c->dec;
+    }
+    cudaEventRecord(a, c->st);
+    for (int i = 0; i < iters; i++) {
+      if (kind == 11)
+        sample_walk_kernel<<<1, SAMPLE_THREADS, 0, c->st>>>(sa);
+      else
+        merge_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_sub, c->d_sub2, c->d_rec, c->n_live, c->next_id);
+      CK_LAUNCH(c);
+    }
+    cudaEventRecord(b, c->st);
+    CK_CUDA(c, cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us = 1e3 * ms / iters;
+    *bytes = kind == 11 ? (double)c->cfg.vocab * 8 : 0.0;   // per walked node: a logits row + a q row
+    return FS_OK;
+  }
 #ifdef FS_DIAG  // timeline diagnostics (build with -DFS_DIAG): probe buffers allocated here
   if (kind == 9 || kind == 10) {
     // diagnostics: phase probes of attention (9) or O-projection GEMM with its
