@@ -1027,6 +1027,38 @@ int layer_forward(fs_ctx* c, int l) {
   return FS_OK;
 }
 
+// the stochastic accept walk (f2): a cluster of SWC CTAs, each with its slice
+// of the vocabulary in shared memory (FS_SAMPLE_ONE_CTA: the single-CTA kernel)
+int launch_sample_walk(fs_ctx* c, const SampleArgs& sa) {
+  if (getenv("FS_SAMPLE_ONE_CTA")) {
+    sample_walk_kernel<<<1, SAMPLE_THREADS, 0, c->st>>>(sa);
+    CK_LAUNCH(c);
+    return FS_OK;
+  }
+  const int per = (c->cfg.vocab + SWC - 1) / SWC;
+  const size_t smem = (size_t)2 * per * sizeof(double);
+  static std::atomic<uint64_t> wattr{0};
+  once_per_device(wattr, c, [] {
+    cudaFuncSetAttribute(sample_walk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(sample_walk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(SWC);
+  lc.blockDim = dim3(SWT);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = c->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = SWC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, sample_walk_cluster_kernel, sa);
+  CK_LAUNCH(c);
+  return FS_OK;
+}
+
 // where the head writes fp32 logits: the per-S-index store in stochastic
 // mode (the walk needs every verified node's distribution), else the
 // caller's parity buffer (or nowhere)
@@ -1673,8 +1705,7 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
       sa.r = c->samp_r;
       sa.qs = c->samp_q;
       sa.dec = c->dec;
-      sample_walk_kernel<<<1, SAMPLE_THREADS, 0, c->st>>>(sa);
-      CK_LAUNCH(c);
+      if ((rc = launch_sample_walk(c, sa))) return rc;
     }
     if (c->logits_buf)   // parity copy of this tick's rows
       CK_CUDA(c, cudaMemcpyAsync(c->logits_buf, c->lstore + (size_t)outseg.b * c->cfg.vocab,
@@ -2050,11 +2081,12 @@ static int bench_kernel_impl(fs_ctx* c, int32_t kind, int32_t iters, double* us,
     }
     cudaEventRecord(a, c->st);
     for (int i = 0; i < iters; i++) {
-      if (kind == 11)
-        sample_walk_kernel<<<1, SAMPLE_THREADS, 0, c->st>>>(sa);
-      else
+      if (kind == 11) {
+        if ((rc = launch_sample_walk(c, sa))) return rc;
+      } else {
         merge_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_sub, c->d_sub2, c->d_rec, c->n_live, c->next_id);
-      CK_LAUNCH(c);
+        CK_LAUNCH(c);
+      }
     }
     cudaEventRecord(b, c->st);
     CK_CUDA(c, cudaEventSynchronize(b));

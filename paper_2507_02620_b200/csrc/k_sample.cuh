@@ -235,6 +235,289 @@ __global__ void __launch_bounds__(SAMPLE_THREADS) sample_walk_kernel(SampleArgs 
   }
 }
 
+
+// ---------------------------------------------------------------- cluster walk
+// The same walk spread over a cluster of SWC CTAs: CTA c keeps its slice of
+// the vocabulary's residual r and draft q in shared memory (fp64), the
+// reductions over V are block reductions combined in rank order through
+// distributed shared memory (deterministic), and every CTA takes the same
+// accept / reject decisions from the same reduced values; rank 0 writes the
+// decision.  One CTA streamed the whole V through L2 for every pass (200 us
+// per 7B walk); here each pass touches V / SWC elements per SM.
+constexpr int SWC = 16;                 // CTAs per walk (non-portable cluster size)
+constexpr int SWT = 512;                // threads per CTA
+
+FS_DEV double ld_dsmem_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+FS_DEV void cluster_sync_acqrel() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// all-reduce of two values over the cluster (sum or max per value), rank order
+template <bool MAX0, bool MAX1>
+FS_DEV void cl_reduce2(double& v0, double& v1, double* sh, double* slot, double* bc) {
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double a0 = __shfl_xor_sync(0xffffffffu, v0, o), a1 = __shfl_xor_sync(0xffffffffu, v1, o);
+    v0 = MAX0 ? fmax(v0, a0) : v0 + a0;
+    v1 = MAX1 ? fmax(v1, a1) : v1 + a1;
+  }
+  __syncthreads();
+  if (lane_id() == 0) {
+    sh[2 * warp_id()] = v0;
+    sh[2 * warp_id() + 1] = v1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b0 = MAX0 ? -INFINITY : 0.0, b1 = MAX1 ? -INFINITY : 0.0;
+    for (int w = 0; w < SWT / 32; w++) {
+      b0 = MAX0 ? fmax(b0, sh[2 * w]) : b0 + sh[2 * w];
+      b1 = MAX1 ? fmax(b1, sh[2 * w + 1]) : b1 + sh[2 * w + 1];
+    }
+    slot[0] = b0;
+    slot[1] = b1;
+  }
+  cluster_sync_acqrel();
+  if (tid == 0) {
+    double b0 = MAX0 ? -INFINITY : 0.0, b1 = MAX1 ? -INFINITY : 0.0;
+    for (int c = 0; c < SWC; c++) {
+      const double x0 = ld_dsmem_f64(dsmem_addr(slot, (uint32_t)c));
+      const double x1 = ld_dsmem_f64(dsmem_addr(slot + 1, (uint32_t)c));
+      b0 = MAX0 ? fmax(b0, x0) : b0 + x0;
+      b1 = MAX1 ? fmax(b1, x1) : b1 + x1;
+    }
+    bc[0] = b0;
+    bc[1] = b1;
+  }
+  cluster_sync_acqrel();   // every slot read before any CTA rewrites it; bc visible
+  v0 = bc[0];
+  v1 = bc[1];
+}
+
+__global__ void __launch_bounds__(SWT) sample_walk_cluster_kernel(SampleArgs a) {
+  extern __shared__ double wsm[];
+  __shared__ double sh[2 * (SWT / 32)];
+  __shared__ double slot[6];   // [0,2) reductions, [2] slice total, [4] sample, [5] its margin
+  __shared__ double bc[2];
+  __shared__ int32_t s_kids[MAXLIVE];
+  __shared__ int s_nk, s_v, s_nacc, s_nflag, s_done, s_pick;
+  const int tid = threadIdx.x;
+  const uint32_t rank = blockIdx.x;     // the grid is one cluster
+  const TreeDev& t = a.t;
+  const int V = a.V, n = a.n_live;
+  const int per = (V + SWC - 1) / SWC;
+  const int lo = min(V, (int)rank * per), hi = min(V, lo + per), ns = hi - lo;
+  double* r = wsm;
+  double* qs = wsm + per;
+  SampleDecision* d = a.dec;
+  if (n <= 0 || !t.verified[0]) {
+    if (rank == 0 && tid == 0) d->progress = 0;
+    return;   // every CTA returns: no cluster barrier follows
+  }
+  if (tid == 0) {
+    s_v = 0;
+    s_nacc = 1;
+    s_nflag = 0;
+    s_done = 0;
+  }
+  if (rank == 0 && tid == 0) d->acc_s[0] = 0;
+  __syncthreads();
+  // the slice owner of token tok and its local index
+  auto ld_r = [&](int tok) { return ld_dsmem_f64(dsmem_addr(r + (tok - (tok / per) * per), (uint32_t)(tok / per))); };
+  auto ld_q = [&](int tok) { return ld_dsmem_f64(dsmem_addr(qs + (tok - (tok / per) * per), (uint32_t)(tok / per))); };
+  while (true) {
+    const int v = s_v;
+    if (tid == 0) s_nk = 0;
+    __syncthreads();
+    if (tid < n && t.par[tid] == v) {
+      int rk = 0;
+      const int my = t.node[tid];
+      for (int j = 0; j < n; j++)
+        if (t.par[j] == v && t.node[j] < my) rk++;
+      s_kids[rk] = tid;
+      atomicAdd(&s_nk, 1);
+    }
+    const float* lg = a.lstore + (size_t)v * V;
+    const float* qv = a.q + (size_t)t.node[v] * V;
+    double m = -INFINITY, dummy = -INFINITY;
+    for (int i = tid; i < ns; i += SWT) m = fmax(m, (double)lg[lo + i] * a.inv_temp);
+    cl_reduce2<true, true>(m, dummy, sh, slot, bc);
+    double z = 0.0, z2 = 0.0;
+    for (int i = tid; i < ns; i += SWT) {
+      const double e = exp((double)lg[lo + i] * a.inv_temp - m);
+      r[i] = e;
+      qs[i] = (double)qv[lo + i];
+      z += e;
+    }
+    cl_reduce2<false, false>(z, z2, sh, slot, bc);
+    for (int i = tid; i < ns; i += SWT) r[i] /= z;
+    cluster_sync_acqrel();   // r normalised in every slice before remote reads
+    const int nk = s_nk;
+    double margin = INFINITY;
+    int acc = -1;
+    for (int k = 0; k < nk; k++) {
+      const int c = s_kids[k];
+      const int tok = t.token[c];
+      const double qt = ld_q(tok);
+      const double ratio = qt > 0.0 ? ld_r(tok) / qt : INFINITY;
+      const double u = sample_uniform(a.seed, t.node[v], k);
+      margin = fmin(margin, fabs(u - ratio));
+      if (u < ratio) {
+        acc = k;
+        break;
+      }
+      cluster_sync_acqrel();   // every CTA read r(tok), q(tok) before the slices change
+      double sr = 0.0, sq = 0.0;
+      for (int i = tid; i < ns; i += SWT) {
+        const double nr = fmax(r[i] - qs[i], 0.0);
+        r[i] = nr;
+        sr += nr;
+        if (lo + i != tok) sq += qs[i];
+      }
+      cl_reduce2<false, false>(sr, sq, sh, slot, bc);
+      for (int i = tid; i < ns; i += SWT) {
+        r[i] /= sr;
+        qs[i] = (lo + i == tok) ? 0.0 : (sq > 0.0 ? qs[i] / sq : qs[i]);
+      }
+      cluster_sync_acqrel();
+    }
+    if (acc < 0) {
+      // x_new ~ residual: cluster prefix over the slice totals, then the owner
+      // slice's block scan (the single-CTA kernel's search, on its slice)
+      const double u = sample_uniform(a.seed, t.node[v], nk);
+      const int pt = (ns + SWT - 1) / SWT;
+      const int b0 = min(ns, tid * pt), b1 = min(ns, b0 + pt);
+      double loc = 0.0;
+      for (int i = b0; i < b1; i++) loc += r[i];
+      // slice total (block sum) published in slot[2]
+      double tot = loc, tdum = 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      __syncthreads();
+      if (lane_id() == 0) sh[warp_id()] = tot;
+      __syncthreads();
+      if (tid == 0) {
+        double b = 0.0;
+        for (int w = 0; w < SWT / 32; w++) b += sh[w];
+        slot[2] = b;
+        slot[5] = 1e300;   // this CTA's sample margin (set by the owner only)
+        s_pick = -1;
+      }
+      (void)tdum;
+      cluster_sync_acqrel();
+      double before = 0.0, total = 0.0;
+      if (tid == 0) {
+        for (int c = 0; c < SWC; c++) {
+          const double x = ld_dsmem_f64(dsmem_addr(slot + 2, (uint32_t)c));
+          if (c < (int)rank) before += x;
+          total += x;
+        }
+        bc[0] = before;
+        bc[1] = total;
+      }
+      __syncthreads();
+      before = bc[0];
+      total = bc[1];
+      const double target = u * total;
+      const double mine = slot[2];
+      if (target >= before && (target < before + mine || (rank == SWC - 1 && !(target < total)))) {
+        // this slice holds the crossing: block inclusive scan of the thread chunks
+        double* scan = sh;   // reuse as [SWT/32] warp totals
+        double incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane_id() >= o) incl += y;
+        }
+        __syncthreads();
+        if (lane_id() == 31) scan[warp_id()] = incl;
+        __syncthreads();
+        double wbefore = 0.0;
+        for (int w = 0; w < warp_id(); w++) wbefore += scan[w];
+        double run = before + wbefore + incl - loc;   // cumulative sum before this thread's chunk
+        if (b0 < b1 && run <= target && target < run + loc) {
+          int pick = lo + b1 - 1;
+          double mg = 0.0;
+          for (int i = b0; i < b1; i++) {
+            const double lo_c = run;
+            run += r[i];
+            if (run > target) {
+              pick = lo + i;
+              mg = fmin(target - lo_c, run - target) / total;
+              break;
+            }
+          }
+          s_pick = pick;
+          bc[0] = mg;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          if (s_pick < 0) {   // rounding moved the crossing out of every chunk: flag
+            s_pick = hi - 1;
+            bc[0] = 0.0;
+          }
+          slot[4] = (double)s_pick;   // publish the sample and its margin
+          slot[5] = bc[0];
+        }
+      }
+      cluster_sync_acqrel();
+      if (rank == 0 && tid == 0) {
+        // the owner: the first CTA (rank order) whose slot[3] was set below 1e300
+        int pick = V - 1;
+        double mg = 0.0;
+        for (int c = 0; c < SWC; c++) {
+          const double mgc = ld_dsmem_f64(dsmem_addr(slot + 5, (uint32_t)c));
+          if (mgc < 1e299) {
+            pick = (int)ld_dsmem_f64(dsmem_addr(slot + 4, (uint32_t)c));
+            mg = mgc;
+            break;
+          }
+        }
+        margin = fmin(margin, mg);
+        if (margin < a.flag) d->flagged[s_nflag++] = v;
+        d->progress = 1;
+        d->n_acc = s_nacc;
+        d->x_new = pick;
+        d->n_new_s = -1;
+        d->cont = 0;
+        d->n_flagged = s_nflag;
+      }
+      cluster_sync_acqrel();   // keep every CTA's shared memory alive for rank 0's reads
+      return;
+    }
+    if (tid == 0) {
+      if (margin < a.flag) s_nflag++;   // the same count in every CTA
+      const int c = s_kids[acc];
+      if (rank == 0 && margin < a.flag) d->flagged[s_nflag - 1] = v;
+      if (!t.verified[c]) {
+        if (rank == 0) {
+          d->progress = 1;
+          d->n_acc = s_nacc;
+          d->x_new = t.token[c];
+          d->n_new_s = c;
+          d->cont = 1;
+          d->n_flagged = s_nflag;
+        }
+        s_done = 1;
+      } else {
+        if (rank == 0) d->acc_s[s_nacc] = c;
+        s_nacc++;
+        s_v = c;
+      }
+    }
+    __syncthreads();
+    if (s_done) {
+      cluster_sync_acqrel();   // no CTA exits while another may still read its slice
+      return;
+    }
+    cluster_sync_acqrel();     // slices are rewritten for the next node
+  }
+}
+
 // Every rank: the broadcast decision -> the accept record (as accept_walk
 // writes it; no prune plan: fs_prune_and_compact reads the rank map back).
 __global__ void apply_decision_kernel(TreeDev t, const SampleDecision* d, TreeRecord* rec) {
