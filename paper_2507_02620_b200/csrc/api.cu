@@ -1743,9 +1743,13 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
       if (acc) {
         apply_decision_kernel<<<1, 256, 0, c->st>>>(c->tree, c->dec, c->d_rec);
         CK_LAUNCH(c);
+        // the prune plan of this decision, so fs_prune_and_compact needs no read-back
+        prune_plan_kernel<<<1, TREE_THREADS, 0, c->st>>>(c->tree, c->d_rec, c->n_live);
+        CK_LAUNCH(c);
       }
       CK_CUDA(c, cudaMemcpyAsync(c->h_rec, c->d_rec, sizeof(TreeRecord), cudaMemcpyDeviceToHost, c->st));
       c->acc_ready = acc;
+      c->plan_ready = acc;
     } else {
       // commit the rows, then the accept walk over the updated tree and the
       // prune plan of its decision (fs_accept / fs_prune_and_compact consume them

@@ -540,7 +540,6 @@ __global__ void apply_decision_kernel(TreeDev t, const SampleDecision* d, TreeRe
     rec->n_new_id = (d->progress && d->n_new_s >= 0) ? t.node[d->n_new_s] : -1;
     rec->cont = d->progress ? d->cont : 0;
     rec->n_flagged = nf;
-    rec->spec_n_pr = -1;
   }
 }
 
