@@ -89,7 +89,8 @@ def test_tiny_random_trees_bubbles(P, l_max):
     gp.close()
 
 
-@pytest.mark.parametrize("name,P", [("small", 2), ("smallq", 2), ("small:4", 4), ("smallq:4", 4)])
+@pytest.mark.parametrize("name,P", [("small", 2), ("smallq", 2), ("small:4", 4), ("smallq:4", 4),
+                                    ("small:8", 8)])
 def test_bf16_local_pipeline_lockstep(name, P):
     """bf16 path (tcgen05 GEMMs, MHA and GQA+bias attention) split over P stages
     on one GPU, planted paths over several segments (mid-flight prunes)."""
