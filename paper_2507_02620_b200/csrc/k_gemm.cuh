@@ -96,6 +96,9 @@ struct GemmEpi {
 #endif
 // NT=64 (the prefill-chunk width): one CTA per SM, a deep ring so the
 // 32 KB stages (weight box + 128-row activation box) keep enough bytes in flight
+#ifndef FS_GEMM_STAGES32
+#define FS_GEMM_STAGES32 6
+#endif
 #ifndef FS_GEMM_STAGES64
 #define FS_GEMM_STAGES64 5
 #endif
@@ -110,7 +113,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // NT=16: 5 stages -> ~110 KB, two CTAs per SM (the next GEMM's CTA starts
   // streaming its weights while this one drains: early PDL trigger)
-  static constexpr int STAGES = NT <= 16 ? FS_GEMM_STAGES16 : (NT <= 32 ? 4 : FS_GEMM_STAGES64);
+  static constexpr int STAGES = NT <= 16 ? FS_GEMM_STAGES16 : (NT <= 32 ? FS_GEMM_STAGES32 : FS_GEMM_STAGES64);
   static constexpr int MIN_CTAS = NT <= 16 ? FS_GEMM_CTAS16 : 1;   // ~110 KB: two CTAs per SM
   // two accumulator buffers (segment s uses buffer s&1) so the MMA of the next
   // tile segment never waits for the epilogue of the previous one
