@@ -22,6 +22,18 @@
 #pragma once
 #include "k_fwd.cuh"
 
+// softmax warps per M-tile: 8 (two threads per query row, one per 64-key half)
+// or 4 (FS_TCA_SPLITROW=0: one thread per row)
+#ifndef FS_TCA_SPLITROW
+#define FS_TCA_SPLITROW 1
+#endif
+// 1: QK^T(j+1) of an M-tile is issued right after P.V(j), relying on the
+// in-order execution of one thread's tcgen05.mma for the P (read by P.V) that
+// QK^T overwrites; 0: wait for P.V(j) to complete first
+#ifndef FS_TCA_ORDERED
+#define FS_TCA_ORDERED 0
+#endif
+
 namespace fs {
 
 constexpr int TCA_KT = 128;              // keys per tile
@@ -29,11 +41,16 @@ constexpr int TCA_BOX = 128 * 128;       // one SW128 box: 128 rows x 64 bf16 = 
 
 template <int MT2>
 struct TcAttnCfg {
-  static constexpr int THREADS = 64 + 128 * MT2;     // producer, MMA, 4 softmax warps per M-tile
+  // producer, MMA, softmax warps: 8 per M-tile (two threads per query row, one
+  // per 64-key half; FS_TCA_SPLITROW=0: 4 per M-tile, one thread per row)
+  static constexpr int SMW = FS_TCA_SPLITROW ? 8 : 4;
+  static constexpr int ROLE_WARPS = 2;   // TMA producer, MMA issuer
+  static constexpr int THREADS = 32 * ROLE_WARPS + 32 * SMW * MT2;
   static constexpr int Q_BYTES = MT2 * 2 * TCA_BOX;   // M-tiles x 2 head-dim boxes
   static constexpr int STAGE_BYTES = 4 * TCA_BOX;     // K (2 boxes) | V (2 boxes)
   static constexpr int NST = 2;
-  static constexpr int SMEM = 1024 + Q_BYTES + NST * STAGE_BYTES + 256 + 2048 + 4 * 128 * MT2;
+  static constexpr int SMEM = 1024 + Q_BYTES + NST * STAGE_BYTES + 256 + 2048 + 4 * 128 * MT2 +
+                              (FS_TCA_SPLITROW ? 6 * 128 * 4 * MT2 + 2048 : 0);   // row-half exchange
   static constexpr int TMEM_COLS = 256 * MT2;         // 256 or 512
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     for (int mi = 0; mi < MT2; mi++) {
       mbar_init(&s_full[mi], 1);
-      mbar_init(&p_full[mi], 128);
+      mbar_init(&p_full[mi], 32 * C::SMW);
       mbar_init(&pv_done[mi], 1);
     }
     mbar_init(&o_full[0], 1);
@@ -186,19 +203,21 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   // context K/V tiles (below the first slot this tick writes) do not depend on
   // the QKV GEMM: the producer streams the first stages before the dependency
   int npre = 0;
+  __shared__ int s_npre;
   if (tid == 0) {
     const int first_written = rows->slot[0];
     const uint64_t pol = l2_evict_first_policy();
     while (npre < min(T, C::NST) && kbeg + (npre + 1) * TCA_KT <= first_written) {
+      const int y = kvh * a.max_ctx + kbeg + npre * TCA_KT;
       mbar_arrive_expect_tx(&full[npre], 4 * TCA_BOX);
       uint8_t* sK = sKV + npre * C::STAGE_BYTES;
-      const int y = kvh * a.max_ctx + kbeg + npre * TCA_KT;
       tma_load_2d(sK, &tmK, &full[npre], 0, y, pol);
       tma_load_2d(sK + TCA_BOX, &tmK, &full[npre], 64, y, pol);
       tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[npre], 0, y, pol);
       tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[npre], 64, y, pol);
       npre++;
     }
+    s_npre = npre;
   }
   // dependents may launch only now: this CTA already holds its TMEM columns
   pdl_trigger();
@@ -245,21 +264,17 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {   // ---------------- TMA producer: K + V tiles
       const uint64_t pol = l2_evict_first_policy();
-      int st = npre % C::NST;
-      uint32_t ph = (uint32_t)((npre / C::NST) & 1);
-      for (int j = npre; j < T; j++) {
-        mbar_wait(&empty[st], ph ^ 1);
+      const int np0 = s_npre;
+      for (int j = np0; j < T; j++) {
+        const int st = j % C::NST;
+        const int y = kvh * a.max_ctx + kbeg + j * TCA_KT;
+        mbar_wait(&empty[st], (uint32_t)(((j / C::NST) & 1) ^ 1));
         mbar_arrive_expect_tx(&full[st], 4 * TCA_BOX);
         uint8_t* sK = sKV + st * C::STAGE_BYTES;
-        const int y = kvh * a.max_ctx + kbeg + j * TCA_KT;
         tma_load_2d(sK, &tmK, &full[st], 0, y, pol);
         tma_load_2d(sK + TCA_BOX, &tmK, &full[st], 64, y, pol);
         tma_load_2d(sK + 2 * TCA_BOX, &tmV, &full[st], 0, y, pol);
         tma_load_2d(sK + 3 * TCA_BOX, &tmV, &full[st], 64, y, pol);
-        if (++st == C::NST) {
-          st = 0;
-          ph ^= 1;
-        }
       }
     }
     __syncwarp();
@@ -276,7 +291,9 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       auto issue_qk = [&](int j, int mi) {
         if (mi == 0) mbar_wait(&full[stage_of(j)], (uint32_t)((j / C::NST) & 1));
         // the S / P columns of M-tile mi are free once P V of tile j-1 read P
+#if !FS_TCA_ORDERED
         if (j > 0) mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));
+#endif
         tc_fence_after();
         const uint32_t k0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES);
         const uint32_t tS = tmem + (uint32_t)(mi * 256);
@@ -317,9 +334,177 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     __syncwarp();
   } else {
+#if FS_TCA_SPLITROW
+    // ---------------- softmax: two threads per query row, one per 64-key half
+    // (warps 8*mi + 4*hf + q): each reads only its half of S and writes only its
+    // half of P; the row maximum (and, at the end, the row sum) is exchanged
+    // through shared memory at one named barrier per tile and M-tile.  The
+    // running maximum M is in raw-score units.
+    const int wi = warp - C::ROLE_WARPS, mi = wi >> 3, hf = (wi >> 2) & 1, q = warp & 3;
+    const int rr = q * 32 + lane, r = mi * 128 + rr;
+    const int m = r % a.npad;
+    const bool live = m < n_rows;
+    const int ctxr = live ? rows->ctx_lim[m] : 0;
+    const int slr = live ? rows->sidx[m] : -1;
+    const int l_glo = rows->l_glo;
+    const int ctx_min = *sCtxMin;
+    const float sc = a.scale_log2;
+    // after the ancestor rows (npad x ancw words, <= 4 KB)
+    float* xmax = reinterpret_cast<float*>(sAnc + a.npad * a.ancw) + (size_t)mi * 6 * 128;   // [2 parity][2 half][128]
+    float* xsum = xmax + 4 * 128;                                                // [2 half][128]
+    const uint32_t lq = ((uint32_t)(q * 32) << 16);
+    const uint32_t tS = tmem + (uint32_t)(mi * 256) + lq + (uint32_t)(hf * 64), tO = tmem + (uint32_t)(mi * 256) + 128 + lq;
+    float M = -INFINITY, L = 0.f;
+    for (int j = 0; j < T; j++) {
+      mbar_wait(&s_full[mi], j & 1);
+      tc_fence_after();
+      if (j == 0) TCA_PROBE(2);
+      if (j == T - 1) TCA_PROBE(6);
+      const int key0 = kbeg + j * TCA_KT + hf * 64;
+      const bool need_mask = !(kbeg + j * TCA_KT + TCA_KT <= min(kend, ctx_min));
+      auto mask16 = [&](float* t, int kb) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+          const int key = kb + i;
+          bool vis = live && key < kend;
+          if (vis && key >= ctxr) {
+            const int aa = key - l_glo;
+            vis = slr >= 0 && aa >= 0 && aa < a.max_live &&
+                  ((sAnc[m * a.ancw + (aa >> 5)] >> (aa & 31)) & 1u);
+          }
+          if (!vis) t[i] = -INFINITY;
+        }
+      };
+      // pass A: the maximum of this half, exchanged with the other half
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        float t[32];
+        tmem_ld16_nw(tS + c * 16, reinterpret_cast<uint32_t*>(t));
+        tmem_ld16_nw(tS + c * 16 + 16, reinterpret_cast<uint32_t*>(t + 16));
+        tmem_ld_wait();
+        if (need_mask) {
+          mask16(t, key0 + c * 16);
+          mask16(t + 16, key0 + c * 16 + 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i++) mx[i & 3] = fmaxf(mx[i & 3], t[i]);
+      }
+      const float mh = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      float* xm = xmax + (j & 1) * 256;
+      xm[hf * 128 + rr] = mh;
+      named_bar_sync(1 + mi, 32 * C::SMW);
+      const float Mn = fmaxf(M, fmaxf(xm[rr], xm[128 + rr]));   // same value in both halves
+      if (j == 0) {
+        M = Mn;
+      } else {
+        const bool resc = Mn != -INFINITY && (M == -INFINITY || (Mn - M) * sc > a.resc_log2);
+        if (__any_sync(0xffffffffu, resc)) {
+          mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));   // O holds tiles < j
+          tc_fence_after();
+          const float f = resc ? ((M == -INFINITY) ? 0.f : ex2_approx((M - Mn) * sc)) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 4; c++) {   // this thread's 64 of the row's 128 O columns
+            uint32_t o[16];
+            const uint32_t to = tO + (uint32_t)(hf * 64 + c * 16);
+            tmem_ld16_nw(to, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+            tmem_st8(to, o);
+            tmem_st8(to + 8, o + 8);
+          }
+          tmem_st_wait();
+          if (resc) {
+            L *= f;
+            M = Mn;
+          }
+        }
+      }
+      // pass B: P of this half into its own S columns (bf16 hi at +0, lo at +32)
+      const float nm = (M == -INFINITY) ? 0.f : -M * sc;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      float sv[64];
+#pragma unroll
+      for (int c = 0; c < 4; c++) tmem_ld16_nw(tS + c * 16, reinterpret_cast<uint32_t*>(sv + c * 16));
+      tmem_ld_wait();
+      if (need_mask)
+#pragma unroll
+        for (int c = 0; c < 4; c++) mask16(sv + c * 16, key0 + c * 16);
+#pragma unroll
+      for (int c16 = 0; c16 < 4; c16++) {
+        uint32_t pk[8], pl[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const int k0 = c16 * 16 + 2 * i;
+          const float x0 = ex2_approx(fmaf(sv[k0], sc, nm)), x1 = ex2_approx(fmaf(sv[k0 + 1], sc, nm));
+          ls[i & 3] += x0 + x1;
+          uint32_t u;
+          if constexpr (PF == TCA_P_F16) {
+            const __half2 hv = __floats2half2_rn(x0, x1);
+            u = *reinterpret_cast<const uint32_t*>(&hv);
+          } else {
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+            u = *reinterpret_cast<const uint32_t*>(&hb);
+          }
+          pk[i] = u;
+          if constexpr (PLO)
+            pl[i] = pack_bf16(x0 - __uint_as_float(u << 16), x1 - __uint_as_float(u & 0xFFFF0000u));
+        }
+        tmem_st8(tS + c16 * 8, pk);
+        if constexpr (PLO) tmem_st8(tS + 32 + c16 * 8, pl);
+      }
+      L += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[mi]);
+    }
+    // ---------------- unnormalised O (this thread's 64 columns) and (M, l)
+    TCA_PROBE(7);
+    mbar_wait(&o_full[mi], 0);
+    tc_fence_after();
+    TCA_PROBE(8);
+    // this M-tile's MMAs have completed; the other M-tile's last P.V may still
+    // read V of the final stage.  M-tile 0 stages in [0, 8*32*68*4) = Q plus K
+    // of stage 0 (last read by the final Q.K^T, issued before any final P.V);
+    // M-tile 1 after it (its o_full follows the kernel's last MMA).
+    constexpr int SLD = 64 + 4;
+    static_assert(MT2 == 1 || 8 * 32 * SLD * 4 <= C::Q_BYTES + 2 * TCA_BOX,
+                  "M-tile 0's output staging would overlap V of stage 0");
+    float* stg = reinterpret_cast<float*>(smem) + (size_t)(wi) * 32 * SLD;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      float o[32];
+      const uint32_t to = tO + (uint32_t)(hf * 64 + c * 32);
+      tmem_ld16_nw(to, reinterpret_cast<uint32_t*>(o));
+      tmem_ld16_nw(to + 16, reinterpret_cast<uint32_t*>(o + 16));
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        *reinterpret_cast<float4*>(stg + lane * SLD + c * 32 + 4 * i) =
+            make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+    }
+    xsum[hf * 128 + rr] = L;
+    __syncwarp();
+    // 16 lanes x float4 = one 256-byte half row; two rows per instruction
+    float* dst = ws_o + (size_t)(r - lane) * ATT_HD + hf * 64;
+#pragma unroll 4
+    for (int row = 0; row < 32; row += 2) {
+      const int rw = row + (lane >> 4), c4 = (lane & 15) * 4;
+      *reinterpret_cast<float4*>(dst + (size_t)rw * ATT_HD + c4) =
+          *reinterpret_cast<const float4*>(stg + rw * SLD + c4);
+    }
+    named_bar_sync(1 + mi, 32 * C::SMW);
+    if (hf == 0) {
+      ws_ml[r * 2] = (M == -INFINITY) ? -INFINITY : M * sc;   // log2 units, as the combine expects
+      ws_ml[r * 2 + 1] = xsum[rr] + xsum[128 + rr];           // half 0 + half 1 (fixed order)
+    }
+    TCA_PROBE(9);
+  }
+#else
     // ---------------- softmax: one thread per query row (TMEM lane quarter
     // warp % 4); the running maximum M is in raw-score units
-    const int wi = warp - 2, mi = wi >> 2, q = warp & 3;
+    const int wi = warp - C::ROLE_WARPS, mi = wi >> 2, q = warp & 3;
     const int rr = q * 32 + lane, r = mi * 128 + rr;
     const int m = r % a.npad;
     const bool live = m < n_rows;
@@ -477,6 +662,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     ws_ml[r * 2 + 1] = L;
     TCA_PROBE(9);
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
