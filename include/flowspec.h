@@ -40,6 +40,9 @@ extern "C" {
 #define FS_ECUDA (-5)      /* CUDA error: context poisoned */
 #define FS_ENCCL (-6)      /* NCCL error: context poisoned */
 #define FS_EPOISONED (-7)  /* an earlier CUDA/NCCL error poisoned the context */
+#define FS_ERANGE (-8)     /* a value outside the range of a kernel-internal format (GQA
+                              attention with fp16 P converts V to fp16: |V| >= 65536 or a
+                              non-finite V); poisons the context */
 
 #define FS_MAX_LIVE 512    /* hard cap on live draft nodes (ancestor bitsets) */
 #define FS_MAX_SEG 64      /* hard cap on rows per segment */
@@ -290,6 +293,12 @@ int fs_query(fs_ctx* ctx, int32_t what, void* buf, size_t bytes, size_t* needed)
  * layer owned by this rank.  FS_EINVAL otherwise. */
 int fs_read_kv(fs_ctx* ctx, int32_t layer, int32_t which, int32_t kv_head,
                int32_t slot, float* out);
+
+/* Test hook: overwrite one K (which=0) or V (which=1) row of a layer owned by
+ * this rank with `in` (head_dim fp32 values, rounded to the cache format,
+ * bf16 round-to-nearest-even).  Synchronous.  FS_EINVAL on a bad index. */
+int fs_debug_write_kv(fs_ctx* ctx, int32_t layer, int32_t which, int32_t kv_head,
+                      int32_t slot, const float* in);
 
 /* ---- measurement ---- */
 typedef struct fs_profile {

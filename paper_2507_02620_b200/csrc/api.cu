@@ -745,6 +745,7 @@ int launch_attention(fs_ctx* c, int l) {
     a.resc_log2 = getenv("FS_TCA_RESCALE") ? (float)atof(getenv("FS_TCA_RESCALE")) : 8.f;
     a.dbg = c->att_dbg;
     a.dbg_ends = c->att_dbg_ends;
+    a.num_err = &c->d_rec->num_err;
     if (c->tl_buf) {
       a.dbg = c->tl_buf + c->tl_names.size() * 8192;
       c->tl_names.push_back("attn");
@@ -891,16 +892,17 @@ int launch_attention(fs_ctx* c, int l) {
       lc.numAttrs = 1;
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
                                            (double)nsplit * Hkv * QR * (hd + 2) * 4 * 2);
-      // P as a bf16 hi/lo pair (default) or plain bf16 (FS_TC_ATTN_P_BF16)
-      // P format of P.V: bf16 hi/lo pair (default), plain bf16 (FS_TC_ATTN_P=bf16: 38.4 vs
-      // 44.5 us per 72B layer but 0.027 > 2e-2 on the logits) or fp16 with V converted to
-      // fp16 in shared memory (FS_TC_ATTN_P=f16; f16 P with bf16 V is not a valid
-      // kind::f16 instruction: A and B formats must match)
+      // P format of P.V: fp16 with V converted to fp16 in shared memory by the softmax
+      // warps (default: one P.V MMA, 72B layer 40.2 us, logits 9.5e-3), the bf16 hi/lo
+      // pair (FS_TC_ATTN_P=hilo: two P.V MMAs, 43.5 us, 9.8e-3) or plain bf16
+      // (FS_TC_ATTN_P=bf16: 38.8 us but 0.027 > 2e-2 on the logits).  f16 P with bf16 V
+      // is not a valid kind::f16 instruction (A and B formats must match); a V outside
+      // fp16's range fails the call with FS_ERANGE
       const char* pfe = getenv("FS_TC_ATTN_P");
       const int pf = getenv("FS_TC_ATTN_P_BF16") ? TCA_P_BF16
-                     : !pfe ? TCA_P_HILO
-                     : !strcmp(pfe, "f16") ? TCA_P_F16
-                     : !strcmp(pfe, "bf16") ? TCA_P_BF16 : TCA_P_HILO;
+                     : !pfe ? TCA_P_F16
+                     : !strcmp(pfe, "hilo") ? TCA_P_HILO
+                     : !strcmp(pfe, "bf16") ? TCA_P_BF16 : TCA_P_F16;
       auto go = [&](auto kern, int threads, int smem_bytes) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         lc.blockDim = dim3(threads);
@@ -1542,7 +1544,13 @@ int fs_set_prefix(fs_ctx* c, const int32_t* tok, int32_t n, int32_t mode, uint64
   {
     const int mlast = n - (start + (n_chunks - 1) * M);
     CK_CUDA(c, cudaMemcpyAsync(c->h_res, c->res, sizeof(RowResult) * mlast, cudaMemcpyDeviceToHost, c->st));
+    CK_CUDA(c, cudaMemcpyAsync(&c->h_rec->num_err, &c->d_rec->num_err, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                               c->st));
     if ((rc = sync(c))) return rc;
+    if (c->h_rec->num_err) {
+      c->poisoned = true;
+      return fail(c, FS_ERANGE, "attention V outside the fp16 range of the f16-P kernel (FS_TC_ATTN_P=hilo)");
+    }
     c->x_new = c->h_res[mlast - 1].am;
   }
   c->l_glo = n;
@@ -1765,6 +1773,10 @@ int fs_verify_step(fs_ctx* c, fs_step_out* out) {
     if (c->h_rec->sub_err) {
       c->poisoned = true;
       return fail(c, FS_EINVAL, "an asynchronous submit was rejected by validation");
+    }
+    if (c->h_rec->num_err) {
+      c->poisoned = true;
+      return fail(c, FS_ERANGE, "attention V outside the fp16 range of the f16-P kernel (FS_TC_ATTN_P=hilo)");
     }
     if (out)
       for (int m = 0; m < n; m++) {
@@ -2010,6 +2022,29 @@ int fs_read_kv(fs_ctx* c, int32_t layer, int32_t which, int32_t kvh, int32_t slo
     }
   }
   return FS_OK;
+}
+
+int fs_debug_write_kv(fs_ctx* c, int32_t layer, int32_t which, int32_t kvh, int32_t slot, const float* in) {
+  int rc;
+  if (!check(c, &rc)) return rc;
+  const fs_config& f = c->cfg;
+  if (!in || layer < c->L0 || layer >= c->L1 || which < 0 || which > 1 || kvh < 0 ||
+      kvh >= f.n_kv_heads || slot < 0 || slot >= f.max_ctx)
+    return fail(c, FS_EINVAL, "bad kv index");
+  char* dst = kv_plane(c, layer - c->L0, which) + ((size_t)kvh * f.max_ctx + slot) * f.head_dim * c->esz;
+  std::vector<char> tmp((size_t)f.head_dim * c->esz);
+  for (int j = 0; j < f.head_dim; j++) {
+    if (c->bf) {
+      uint32_t u;
+      memcpy(&u, &in[j], 4);
+      u += 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even (finite inputs)
+      ((uint16_t*)tmp.data())[j] = (uint16_t)(u >> 16);
+    } else {
+      ((float*)tmp.data())[j] = in[j];
+    }
+  }
+  CK_CUDA(c, cudaMemcpyAsync(dst, tmp.data(), tmp.size(), cudaMemcpyHostToDevice, c->st));
+  return sync(c);
 }
 
 int fs_set_profiling(fs_ctx* c, int32_t on) {
@@ -2466,6 +2501,7 @@ const char* fs_strerror(int code) {
     case FS_ECUDA: return "CUDA error (context poisoned)";
     case FS_ENCCL: return "NCCL error (context poisoned)";
     case FS_EPOISONED: return "context poisoned by an earlier CUDA/NCCL error";
+    case FS_ERANGE: return "value outside a kernel-internal format's range (context poisoned)";
   }
   return "unknown error";
 }

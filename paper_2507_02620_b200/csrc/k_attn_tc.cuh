@@ -112,6 +112,12 @@ FS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::c
 // P formats of the P.V MMA: bf16, bf16 hi + lo pair (two MMAs), fp16 (A f16
 // from TMEM with B = V bf16 in the same kind::f16 instruction)
 constexpr int TCA_P_BF16 = 0, TCA_P_HILO = 1, TCA_P_F16 = 2;
+// nonzero if either bf16 of the pair is outside fp16's finite range (biased
+// exponent >= 127 + 16: |v| >= 65536; every bf16 below converts finitely) or
+// not finite
+FS_DEV uint32_t f16_range_check(uint32_t x) {
+  return (uint32_t)(((x >> 7) & 0xFFu) >= 143u) | (uint32_t)(((x >> 23) & 0xFFu) >= 143u);
+}
 
 template <int MT2, int PF>
 __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
@@ -143,8 +149,18 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     if (a.dbg && threadIdx.x == 64)                                                        \
       a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = gtimer();          \
   } while (0)
+// accumulated durations: slot k = this CTA's start + the sum (the host prints
+// offsets from the earliest CTA start)
+#define TCA_T() gtimer()
+#define TCA_ACC(cond, k, v)                                                                 \
+  do {                                                                                     \
+    if (a.dbg && (cond)) a.dbg[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (k)] = t_cta0 + (v); \
+  } while (0)
+  const unsigned long long t_cta0 = gtimer();
 #else
 #define TCA_PROBE(k) do {} while (0)
+#define TCA_T() 0ull
+#define TCA_ACC(cond, k, v) do {} while (0)
 #endif
   TCA_PROBE(0);
   const TickRows* rows = a.rows;
@@ -178,7 +194,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     }
     mbar_init(&o_full[0], 1);
     mbar_init(&o_full[1], 1);
-    for (int st = 0; st < C::NST; st++) mbar_init(&v_ready[st], 62);
+    for (int st = 0; st < C::NST; st++) mbar_init(&v_ready[st], FS_TCA_SPLITROW ? 32 * C::SMW * MT2 : 62);
     fence_barrier_init();
   }
   const int n_rows = rows->n_rows;
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
   __syncthreads();
   TCA_PROBE(1);
 
-  if constexpr (PF == TCA_P_F16) {
+  if constexpr (PF == TCA_P_F16 && !FS_TCA_SPLITROW) {
     if (warp <= 1 && lane > 0) {
       // ---------------- V bf16 -> fp16 in place (62 lanes of the producer and MMA
       // warps): element-wise, so the SW128 layout the MMA reads is unchanged;
@@ -288,12 +304,17 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       const uint32_t q0 = smem_u32(sQ);
       const uint32_t kv0 = smem_u32(sKV);
       auto stage_of = [&](int j) { return j % C::NST; };
+      unsigned long long w_p = 0, w_full = 0, w_pv = 0;
       auto issue_qk = [&](int j, int mi) {
+        unsigned long long t0 = TCA_T();
         if (mi == 0) mbar_wait(&full[stage_of(j)], (uint32_t)((j / C::NST) & 1));
+        unsigned long long t1 = TCA_T();
+        w_full += t1 - t0;
         // the S / P columns of M-tile mi are free once P V of tile j-1 read P
 #if !FS_TCA_ORDERED
         if (j > 0) mbar_wait(&pv_done[mi], (uint32_t)((j - 1) & 1));
 #endif
+        w_pv += TCA_T() - t1;
         tc_fence_after();
         const uint32_t k0 = kv0 + (uint32_t)(stage_of(j) * C::STAGE_BYTES);
         const uint32_t tS = tmem + (uint32_t)(mi * 256);
@@ -306,7 +327,9 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
         umma_commit(&s_full[mi]);
       };
       auto issue_pv = [&](int j, int mi) {
+        unsigned long long t0 = TCA_T();
         mbar_wait(&p_full[mi], (uint32_t)(j & 1));   // P of this tile written (and O rescaled)
+        w_p += TCA_T() - t0;
         if constexpr (PF == TCA_P_F16)
           if (mi == 0) mbar_wait(&v_ready[stage_of(j)], (uint32_t)((j / C::NST) & 1));
         tc_fence_after();
@@ -331,6 +354,9 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
         }
         umma_commit(&empty[stage_of(j)]);   // stage j's K / V reads are all issued
       }
+      TCA_ACC(true, 3, w_p);
+      TCA_ACC(true, 4, w_full);
+      TCA_ACC(true, 5, w_pv);
     }
     __syncwarp();
   } else {
@@ -355,9 +381,38 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
     const uint32_t lq = ((uint32_t)(q * 32) << 16);
     const uint32_t tS = tmem + (uint32_t)(mi * 256) + lq + (uint32_t)(hf * 64), tO = tmem + (uint32_t)(mi * 256) + 128 + lq;
     float M = -INFINITY, L = 0.f;
+    unsigned long long w_s = 0, b_s = 0, t_arr = 0;
     for (int j = 0; j < T; j++) {
+      const unsigned long long tw0 = TCA_T();
+      if constexpr (PF == TCA_P_F16) {
+        // V(j) bf16 -> fp16 in place while S(j) is computed: this M-tile's
+        // threads convert their half of the stage's V boxes (element-wise, the
+        // SW128 layout the MMA reads is unchanged; exact for |v| in fp16's
+        // normal range [2^-14, 65504], smaller values keep their fp16-subnormal
+        // part, an absolute error below 2^-25)
+        const int st = j % C::NST;
+        mbar_wait(&full[st], (uint32_t)((j / C::NST) & 1));
+        uint4* v = reinterpret_cast<uint4*>(sKV + st * C::STAGE_BYTES + 2 * TCA_BOX) + mi * (2 * TCA_BOX / 16 / MT2);
+        const int ti = wi % 8 * 32 + lane;
+        uint32_t ovf = 0;
+#pragma unroll
+        for (int i = ti; i < 2 * TCA_BOX / 16 / MT2; i += 32 * C::SMW) {
+          uint4 x = v[i];
+          ovf |= f16_range_check(x.x) | f16_range_check(x.y) | f16_range_check(x.z) | f16_range_check(x.w);
+          x.x = bf16x2_to_f16x2(x.x);
+          x.y = bf16x2_to_f16x2(x.y);
+          x.z = bf16x2_to_f16x2(x.z);
+          x.w = bf16x2_to_f16x2(x.w);
+          v[i] = x;
+        }
+        fence_proxy_async_smem();   // the MMA reads V through the async proxy
+        mbar_arrive(&v_ready[st]);
+        if (ovf) *a.num_err = 1;   // fails the call loudly (FS_ERANGE), no silent inf
+      }
       mbar_wait(&s_full[mi], j & 1);
       tc_fence_after();
+      const unsigned long long tw1 = TCA_T();
+      w_s += tw1 - tw0;
       if (j == 0) TCA_PROBE(2);
       if (j == T - 1) TCA_PROBE(6);
       const int key0 = kbeg + j * TCA_KT + hf * 64;
@@ -458,7 +513,11 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[mi]);
+      t_arr = TCA_T();
+      b_s += t_arr - tw1;
     }
+    TCA_ACC(wi % 8 == 0 && lane == 0, 10 + 2 * mi, w_s);
+    TCA_ACC(wi % 8 == 0 && lane == 0, 11 + 2 * mi, b_s);
     // ---------------- unnormalised O (this thread's 64 columns) and (M, l)
     TCA_PROBE(7);
     mbar_wait(&o_full[mi], 0);

@@ -232,6 +232,7 @@ struct AttnArgs {
                         // than 2^resc_log2 (8; FS_TCA_RESCALE overrides, 0 = at every increase: tests)
   unsigned long long* dbg;  // optional phase timestamps [cta][16] (diagnostics)
   int dbg_ends;             // diagnostics: record only the first and last probe
+  int32_t* num_err;         // sticky range flag (TreeRecord::num_err)
 };
 FS_DEV unsigned long long gtimer() {
   unsigned long long t;

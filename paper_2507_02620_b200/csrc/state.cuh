@@ -55,6 +55,7 @@ struct TreeRecord {
   int32_t n_pr;             // |I_pr| (prune)
   int32_t n_batch;          // merge: nodes of T_new whose path is new (ids base .. base+n_batch-1)
   int32_t sub_err;          // sticky: an asynchronous submit's validation error (read by the next verify)
+  int32_t num_err;          // sticky: a value outside a kernel-internal format's range (fp16 V of the f16-P attention)
   int32_t order[MAXLIVE];   // submit: batch node ids in S order
   int32_t merged[MAXLIVE];  // merge: node id of every T_new node (existing or new)
   int32_t acc_s[MAXLIVE];   // accept: S indices of S_acc

@@ -13,8 +13,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO = os.path.join(HERE, "libflowspec.so")
 
-FS_OK, FS_EINVAL, FS_ENOMEM, FS_ESTATE, FS_ECAPACITY, FS_ECUDA, FS_ENCCL, FS_EPOISONED = \
-    0, -1, -2, -3, -4, -5, -6, -7
+FS_OK, FS_EINVAL, FS_ENOMEM, FS_ESTATE, FS_ECAPACITY, FS_ECUDA, FS_ENCCL, FS_EPOISONED, FS_ERANGE = \
+    0, -1, -2, -3, -4, -5, -6, -7, -8
 FS_MAX_LIVE, FS_MAX_SEG, FS_MAX_STAGES = 512, 64, 8
 FS_PREFILL, FS_SYNTH_KV = 0, 1
 FS_NEW_ROUND, FS_APPEND = 1, 2
@@ -70,7 +70,7 @@ class fs_profile(C.Structure):
 EXPORTS = ["fs_layers_per_stage", "fs_debug_gemm", "fs_bench_kernel", "fs_set_profiling", "fs_get_profile", "fs_arena_bytes", "fs_nccl_unique_id", "fs_init", "fs_load_random_weights",
            "fs_set_prefix", "fs_submit_segment", "fs_verify_step", "fs_set_logits_buffer",
            "fs_accept", "fs_prune_and_compact", "fs_query", "fs_read_kv", "fs_destroy",
-           "fs_last_error", "fs_strerror", "fs_local_group_create", "fs_local_group_destroy", "fs_set_acceptance"]
+           "fs_last_error", "fs_strerror", "fs_local_group_create", "fs_local_group_destroy", "fs_set_acceptance", "fs_debug_write_kv"]
 EXPORTS.sort()
 
 _lib = None
@@ -100,6 +100,7 @@ def lib():
         L.fs_prune_and_compact.argtypes = [P, C.POINTER(fs_accept_out)]
         L.fs_query.argtypes = [P, i32, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
         L.fs_read_kv.argtypes = [P, i32, i32, i32, i32, C.POINTER(C.c_float)]
+        L.fs_debug_write_kv.argtypes = [P, i32, i32, i32, i32, C.POINTER(C.c_float)]
         L.fs_set_profiling.argtypes = [P, i32]
         L.fs_get_profile.argtypes = [P, C.POINTER(fs_profile)]
         L.fs_bench_kernel.argtypes = [P, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
@@ -319,6 +320,12 @@ class Pipeline:
                                        X.shape[0], C.cast(Y.data_ptr(), C.POINTER(C.c_float))),
                   "fs_debug_gemm")
         return Y.cpu().numpy()
+
+    def debug_write_kv(self, layer, which, kvh, slot, row):
+        row = np.ascontiguousarray(row, dtype=np.float32)
+        assert row.shape == (self.shape.head_dim,)
+        self._chk(self.L.fs_debug_write_kv(self.h, layer, which, kvh, slot,
+                                           row.ctypes.data_as(C.POINTER(C.c_float))), "fs_debug_write_kv")
 
     def read_kv(self, layer, which, kvh, slot):
         out = np.zeros(self.shape.head_dim, np.float32)

@@ -82,3 +82,44 @@ def test_72b_gqa_online_softmax_rescale_path(monkeypatch):
     against the oracle on the configs[4] per-layer shapes."""
     monkeypatch.setenv("FS_TCA_RESCALE", "0")
     _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
+
+
+def test_72b_gqa_hilo_p_path(monkeypatch):
+    """The bf16 hi/lo P variant of the GQA kernel (two P.V MMAs, bf16 V) stays
+    selectable (FS_TC_ATTN_P=hilo) and parity-green on the configs[4] shapes."""
+    monkeypatch.setenv("FS_TC_ATTN_P", "hilo")
+    _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
+
+
+@pytest.mark.parametrize("pf", ["f16", "hilo"])
+def test_72b_gqa_fp16_v_range_fails_loudly(monkeypatch, pf):
+    """The default GQA kernel converts V tiles to fp16 in shared memory: a V
+    row outside fp16's range (|v| >= 65536) must fail the verify step with
+    FS_ERANGE (and poison the context), never produce a silent inf; the hi/lo
+    variant reads bf16 V directly and accepts the same row."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2507_02620_b200 import flowspec as F
+    monkeypatch.setenv("FS_TC_ATTN_P", pf)
+    shape = SHAPES["72b_l2"]
+    gp = F.Pipeline(shape, max_ctx=1024, max_seg=32)
+    gp.fs_load_random_weights(SEED)
+    prefix = gen.prefix_tokens(SEED, 300, shape.vocab)
+    gp.fs_set_prefix(prefix, F.FS_SYNTH_KV, kv_seed=7)
+    row = gp.read_kv(0, 1, 3, 17)
+    row[5] = 1.0e5
+    gp.debug_write_kv(0, 1, 3, 17, row)
+    assert gp.read_kv(0, 1, 3, 17)[5] > 65536
+    tree = gen.random_tree(3, 32, 6, shape.vocab, gp.state()["x_new"])
+    gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], 32)
+    if pf == "hilo":
+        r = gp.fs_verify_step()
+        assert r["n_rows"] == 32
+        return
+    with pytest.raises(F.FlowSpecError) as e:
+        gp.fs_verify_step()
+    assert e.value.code == F.FS_ERANGE
+    with pytest.raises(F.FlowSpecError) as e:
+        gp.fs_verify_step()
+    assert e.value.code == F.FS_EPOISONED
