@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(MHA_THREADS) attn_mha_tma_kernel(const __grid_
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  mha_flag_range<KPW>(w, a);
   // ---- merge the key-warps of each m-tile (the ring is free: every stage consumed)
   float* so = reinterpret_cast<float*>(sRing);
   float* sPart = so + 4 * 16 * ATT_SO_LD + 4 * 16 * 2;

@@ -112,12 +112,6 @@ FS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::c
 // P formats of the P.V MMA: bf16, bf16 hi + lo pair (two MMAs), fp16 (A f16
 // from TMEM with B = V bf16 in the same kind::f16 instruction)
 constexpr int TCA_P_BF16 = 0, TCA_P_HILO = 1, TCA_P_F16 = 2;
-// nonzero if either bf16 of the pair is outside fp16's finite range (biased
-// exponent >= 127 + 16: |v| >= 65536; every bf16 below converts finitely) or
-// not finite
-FS_DEV uint32_t f16_range_check(uint32_t x) {
-  return (uint32_t)(((x >> 7) & 0xFFu) >= 143u) | (uint32_t)(((x >> 23) & 0xFFu) >= 143u);
-}
 
 template <int MT2, int PF>
 __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)

@@ -205,6 +205,12 @@ FS_DEV uint32_t bf16x2_to_f16x2(uint32_t v) {
   const __half2 h = __floats2half2_rn(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// nonzero if either bf16 of the pair is outside fp16's finite range (biased
+// exponent >= 127 + 16: |v| >= 65536; every smaller bf16 converts finitely) or
+// not finite: the fp16 P.V paths flag it (AttnArgs::num_err -> FS_ERANGE)
+FS_DEV uint32_t f16_range_check(uint32_t x) {
+  return (uint32_t)(((x >> 7) & 0xFFu) >= 143u) | (uint32_t)(((x >> 23) & 0xFFu) >= 143u);
+}
 #ifndef FS_MHA_P16
 #define FS_MHA_P16 1
 #endif
@@ -535,6 +541,19 @@ FS_DEV void mha_warp_init(MhaWarp<KPW>& w, const AttnArgs& a, int warp, int lane
   for (int j = 0; j < 16; j++) w.oacc[j][0] = w.oacc[j][1] = w.oacc[j][2] = w.oacc[j][3] = 0.f;
   w.mrow[0] = w.mrow[1] = -INFINITY;
   w.lrow[0] = w.lrow[1] = 0.f;
+}
+// after the key loop: a V outside fp16's range became inf in the fp16 P.V
+// (inf, or NaN where P = 0) and stays non-finite in the fp32 accumulator, so
+// one check of the accumulators flags it (fails the call loudly) without a
+// per-fragment test in the inner loop
+template <int KPW>
+FS_DEV void mha_flag_range(const MhaWarp<KPW>& w, const AttnArgs& a) {
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 16; j++)
+#pragma unroll
+    for (int e = 0; e < 4; e++) bad |= !isfinite(w.oacc[j][e]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && a.num_err) *a.num_err = 1;
 }
 
 // Q fragments of the warp's m-tile into registers (once)
@@ -908,6 +927,7 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
     if (issued < nsc) load_sub(issued++);
   }
   ATT_PROBE(10);
+  mha_flag_range<KPW>(w, a);
   // ---- merge the KS key-warps of each m-tile (shared memory)
   mha_ks_merge<KPW>(w, a, reinterpret_cast<float*>(sKV), sPart, sPml, tid, warp, lane, 0);
   // ---- cluster merge of the splits through distributed shared memory:

@@ -91,31 +91,37 @@ def test_72b_gqa_hilo_p_path(monkeypatch):
     _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
 
 
-@pytest.mark.parametrize("pf", ["f16", "hilo"])
-def test_72b_gqa_fp16_v_range_fails_loudly(monkeypatch, pf):
-    """The default GQA kernel converts V tiles to fp16 in shared memory: a V
-    row outside fp16's range (|v| >= 65536) must fail the verify step with
-    FS_ERANGE (and poison the context), never produce a silent inf; the hi/lo
-    variant reads bf16 V directly and accepts the same row."""
+@pytest.mark.parametrize("name,seg,env,fails", [
+    ("72b_l2", 32, {}, True),                          # GQA tcgen05 kernel, fp16 P (default)
+    ("72b_l2", 32, {"FS_TC_ATTN_P": "hilo"}, False),   # GQA, bf16 hi/lo P: reads bf16 V directly
+    ("7b_l2", 16, {}, True),                           # MHA cluster kernel, fp16 P.V fragments
+    ("7b_l2", 16, {"FS_MHA_TMA": "1"}, True),          # MHA TMA-ring kernel
+])
+def test_fp16_pv_v_range_fails_loudly(monkeypatch, name, seg, env, fails):
+    """The fp16 P.V paths convert V (bf16) to fp16 on chip: a V row outside
+    fp16's range (|v| >= 65536) must fail the verify step with FS_ERANGE (and
+    poison the context), never produce a silent inf; the GQA hi/lo variant
+    reads bf16 V directly and accepts the same row."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from paper_2507_02620_b200 import flowspec as F
-    monkeypatch.setenv("FS_TC_ATTN_P", pf)
-    shape = SHAPES["72b_l2"]
-    gp = F.Pipeline(shape, max_ctx=1024, max_seg=32)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    shape = SHAPES[name]
+    gp = F.Pipeline(shape, max_ctx=1024, max_seg=seg)
     gp.fs_load_random_weights(SEED)
     prefix = gen.prefix_tokens(SEED, 300, shape.vocab)
     gp.fs_set_prefix(prefix, F.FS_SYNTH_KV, kv_seed=7)
-    row = gp.read_kv(0, 1, 3, 17)
+    kvh = min(3, shape.n_kv_heads - 1)
+    row = gp.read_kv(0, 1, kvh, 17)
     row[5] = 1.0e5
-    gp.debug_write_kv(0, 1, 3, 17, row)
-    assert gp.read_kv(0, 1, 3, 17)[5] > 65536
-    tree = gen.random_tree(3, 32, 6, shape.vocab, gp.state()["x_new"])
-    gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], 32)
-    if pf == "hilo":
-        r = gp.fs_verify_step()
-        assert r["n_rows"] == 32
+    gp.debug_write_kv(0, 1, kvh, 17, row)
+    assert gp.read_kv(0, 1, kvh, 17)[5] > 65536
+    tree = gen.random_tree(3, seg, 6, shape.vocab, gp.state()["x_new"])
+    gp.fs_submit_segment(F.FS_NEW_ROUND, tree["parent"], tree["token"], tree["own"], seg)
+    if not fails:
+        assert gp.fs_verify_step()["n_rows"] == seg
         return
     with pytest.raises(F.FlowSpecError) as e:
         gp.fs_verify_step()
