@@ -721,6 +721,25 @@ char* kv_plane(fs_ctx* c, int local_layer, int which) {
   return c->kv + ((size_t)local_layer * 2 + which) * c->kv_plane_elems * c->esz;
 }
 
+// merge of the split partials (programmatic launch): one warp per (row, head),
+// or one CTA per (row, head) (FS_COMBINE_CTA)
+void launch_combine(fs_ctx* c, const AttnArgs& a, cudaLaunchAttribute* pdl, int nsplit) {
+  static const bool cta = getenv("FS_COMBINE_CTA") != nullptr;
+  cudaLaunchConfig_t cc = {};
+  cc.stream = c->st;
+  cc.attrs = pdl;
+  cc.numAttrs = 1;
+  if (cta) {
+    cc.gridDim = dim3(c->npad, c->cfg.n_heads);
+    cc.blockDim = dim3(ATT_HD);
+    cudaLaunchKernelEx(&cc, attn_combine_kernel, a, (bf16*)c->att, 1, nsplit);
+  } else {
+    cc.gridDim = dim3(c->npad, (c->cfg.n_heads + 3) / 4);
+    cc.blockDim = dim3(128);
+    cudaLaunchKernelEx(&cc, attn_combine_warp_kernel, a, (bf16*)c->att, nsplit);
+  }
+}
+
 // tree-masked attention of local layer l on the current rows -> c->att (hi/lo)
 int launch_attention(fs_ctx* c, int l) {
   const fs_config& f = c->cfg;
@@ -802,13 +821,7 @@ int launch_attention(fs_ctx* c, int l) {
       else
         cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<32>, c->lw[l].mk, c->lw[l].mv, a);
       CK_LAUNCH(c);
-      cudaLaunchConfig_t cc = {};
-      cc.gridDim = dim3(np, H);
-      cc.blockDim = dim3(ATT_HD);
-      cc.stream = c->st;
-      cc.attrs = at;
-      cc.numAttrs = 1;
-      cudaLaunchKernelEx(&cc, attn_combine_kernel, a, (bf16*)c->att, 1, nsplit);
+      launch_combine(c, a, at, nsplit);
       prof_end(c, api);
       CK_LAUNCH(c);
     } else if (MT <= 2) {
@@ -920,13 +933,7 @@ int launch_attention(fs_ctx* c, int l) {
       }
       prof_end(c, api);
       CK_LAUNCH(c);
-      cudaLaunchConfig_t cc = {};
-      cc.gridDim = dim3(np, H);
-      cc.blockDim = dim3(ATT_HD);
-      cc.stream = c->st;
-      cc.attrs = at;   // programmatic dependent launch
-      cc.numAttrs = 1;
-      cudaLaunchKernelEx(&cc, attn_combine_kernel, a, (bf16*)c->att, 1, nsplit);
+      launch_combine(c, a, at, nsplit);
       CK_LAUNCH(c);
       return FS_OK;
     }

@@ -481,6 +481,79 @@ __global__ void attn_combine_kernel(AttnArgs a, bf16* out, int ks, int n_parts_f
   out[((size_t)(a.npad + m) * a.H + h) * ATT_HD + j] = __float2bfloat16_rn(o - __bfloat162float(hi));
 }
 
+// The same merge with one warp per (row, head): lane i reads split i's (m, l)
+// (one coalesced load for up to 32 splits), the maximum and the weighted sum
+// come from warp shuffles, and every lane accumulates its float4 of the 128
+// dims over the splits in split order with all O loads of a batch in flight.
+// Deterministic (fixed shuffle tree, fixed split order).  CTA = 4 heads of one
+// row; grid (npad, H / 4).
+__global__ void __launch_bounds__(128) attn_combine_warp_kernel(AttnArgs a, bf16* out, int n_parts) {
+  const int m = blockIdx.x, h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  pdl_trigger();   // the next kernel streams its weights meanwhile
+  if (m >= a.rows->n_rows || h >= a.H) return;
+  const int G = a.H / a.Hkv;
+  const int kvh = h / G, g = h % G;
+  const int QR = G * a.npad;
+  const int r = g * a.npad + m;
+  pdl_wait();      // the split partials come from the attention kernel
+  auto base_of = [&](int i) { return ((size_t)i * a.Hkv + kvh) * QR + r; };
+  // maximum over the splits (log2 units; -inf marks an empty split)
+  float M = -INFINITY;
+  for (int i0 = 0; i0 < n_parts; i0 += 32) {
+    const float mi = (i0 + lane < n_parts) ? a.ws_ml[base_of(i0 + lane) * 2] : -INFINITY;
+    M = fmaxf(M, mi);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < n_parts; i0 += 32) {
+    float w = 0.f;
+    if (i0 + lane < n_parts) {
+      const float mi = a.ws_ml[base_of(i0 + lane) * 2];
+      if (mi != -INFINITY) {
+        w = exp2f(mi - M);
+        L += a.ws_ml[base_of(i0 + lane) * 2 + 1] * w;
+      }
+    }
+    const int nb = min(32, n_parts - i0);
+    constexpr int B = 8;
+    for (int b0 = 0; b0 < nb; b0 += B) {
+      float4 o[B];
+      float wi[B];
+#pragma unroll
+      for (int k = 0; k < B; k++) {
+        wi[k] = __shfl_sync(0xffffffffu, w, (b0 + k) & 31);
+        o[k] = (b0 + k < nb && wi[k] != 0.f)
+                   ? *reinterpret_cast<const float4*>(a.ws_o + base_of(i0 + b0 + k) * ATT_HD + lane * 4)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int k = 0; k < B; k++) {
+        if (b0 + k >= nb || wi[k] == 0.f) continue;
+        acc.x += o[k].x * wi[k];
+        acc.y += o[k].y * wi[k];
+        acc.z += o[k].z * wi[k];
+        acc.w += o[k].w * wi[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  const float inv = 1.f / L;
+  const float v[4] = {acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv};
+  uint32_t hi2[2], lo2[2];
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    const __nv_bfloat162 hb = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+    hi2[k] = *reinterpret_cast<const uint32_t*>(&hb);
+    lo2[k] = pack_bf16(v[2 * k] - __bfloat162float(hb.x), v[2 * k + 1] - __bfloat162float(hb.y));
+  }
+  *reinterpret_cast<uint2*>(out + ((size_t)m * a.H + h) * ATT_HD + lane * 4) = make_uint2(hi2[0], hi2[1]);
+  *reinterpret_cast<uint2*>(out + ((size_t)(a.npad + m) * a.H + h) * ATT_HD + lane * 4) =
+      make_uint2(lo2[0], lo2[1]);
+}
+
 // ---------------------------------------------------------------- MHA attention
 // Segment rows x heads with G*npad <= 32 query rows per kv head (MHA configs).
 // CTA = (key split, kv head); the nsplit (<= 8) splits of one kv head form a
