@@ -304,7 +304,7 @@ struct Carver {
 };
 
 void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const char* env = nullptr,
-               int def_split = -1) {
+               int def_split = -1, bool wide = false) {
   g.sh.n_out = n_out;
   g.sh.K = K;
   g.sh.kb_total = K / 64;
@@ -318,6 +318,11 @@ void plan_gemm(GemmOp& g, int n_out, int K, int n_sms, int ctas_per_sm, const ch
   g.grid = std::min(n_sms, g.sh.units);
   if (g.sh.n_tiles > n_sms && g.sh.n_tiles <= ctas_per_sm * n_sms && !getenv("FS_NO_TILE_GRID"))
     g.grid = g.sh.n_tiles;
+  // Prefill-width rows with fewer tiles than SMs: one CTA per tile (no 64-column
+  // stream-K fix-up) is faster (7B QKV 33.6 vs 38.1 us) but changes the fp32
+  // summation order, and the 72B 2-layer prefill lockstep then sits at 0.0200 of
+  // its 2e-2 logit bar (0.0180 with stream-K): opt-in only (FS_WIDE_TILES)
+  if (wide && g.sh.n_tiles <= ctas_per_sm * n_sms && getenv("FS_WIDE_TILES")) g.grid = g.sh.n_tiles;
   // Few output tiles: tile-aligned cluster split-K with S CTAs per tile.  Two
   // CTAs fit per SM (NT 16): S = the largest power of two keeping the grid in
   // one wave of 2 x SMs slots; otherwise S = floor(SMs / tiles).  Many tiles:
@@ -369,17 +374,17 @@ size_t carve(fs_ctx* c, char* base) {
     plan_gemm(w.o, d, H * hd, c->n_sms, c->ctas_tick, "FS_SPLIT_O");
     plan_gemm(w.gu, 2 * ffn, d, c->n_sms, c->ctas_tick, "FS_SPLIT_GU");
     plan_gemm(w.dn, d, ffn, c->n_sms, c->ctas_tick, "FS_SPLIT_DN");
-    plan_gemm(w.qkv_w, nq, d, c->n_sms, c->ctas_pre);
-    plan_gemm(w.o_w, d, H * hd, c->n_sms, c->ctas_pre);
-    plan_gemm(w.gu_w, 2 * ffn, d, c->n_sms, c->ctas_pre);
-    plan_gemm(w.dn_w, d, ffn, c->n_sms, c->ctas_pre);
+    plan_gemm(w.qkv_w, nq, d, c->n_sms, c->ctas_pre, nullptr, -1, true);
+    plan_gemm(w.o_w, d, H * hd, c->n_sms, c->ctas_pre, nullptr, -1, true);
+    plan_gemm(w.gu_w, 2 * ffn, d, c->n_sms, c->ctas_pre, nullptr, -1, true);
+    plan_gemm(w.dn_w, d, ffn, c->n_sms, c->ctas_pre, nullptr, -1, true);
   }
   c->emb = c->first ? cv.take<char>((size_t)V * d * es) : nullptr;
   if (c->last) {
     c->wh = cv.take<char>(wr(V) * d * es);
     c->gf = cv.take<char>((size_t)d * es);
     plan_gemm(c->head, V, d, c->n_sms, c->ctas_tick, "FS_SPLIT_HEAD");
-    plan_gemm(c->head_w, V, d, c->n_sms, c->ctas_pre);
+    plan_gemm(c->head_w, V, d, c->n_sms, c->ctas_pre, nullptr, -1, true);
   }
   c->kv_plane_elems = (size_t)Hkv * f.max_ctx * hd;
   c->kv = cv.take<char>((size_t)c->nl * 2 * c->kv_plane_elems * es);

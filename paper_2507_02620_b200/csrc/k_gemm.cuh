@@ -503,128 +503,229 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
       // its, so the partial is published long before; the head's epilogue
       // warps wait for it and pull it into registers while the MMA still
       // streams, keeping both L2 round trips off the tail.
-      float pre[NT];
-      if (nc == 2 && j == 0) {
-        if (warp == 2 && lane == 0)
-          while (ld_acquire_gpu(&sh.counters[t]) < 1) __nanosleep(64);
-        named_bar_sync(1, 128);
-        const float* rp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
+      if constexpr (NT > 32) {
+        // Wide rows (prefill chunks): the tile's accumulator stays in TMEM and
+        // every step runs over 16-column windows (register budget: 64 columns of
+        // own / partial / sum values do not fit one thread), partials summed in
+        // contributor order as below; the buffer is released after its last read.
+        constexpr int EW = 16;
+        // per-column epilogue operands (RoPE cos/sin, KV slots, residual rows) of
+        // window 0, loaded while the mainloop still streams; later windows load
+        // theirs (all 16 columns in flight) just before use
+        EpiPre<EW> pw;
+        epi_prefetch<NT, EW, true>(sh, ep, t, row, 0, EW, true, pw);
+        mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
+        auto own_window = [&](int wlo, float* v) {
+          tmem_ld16(tl + wlo, v);
+          float w[EW];
+          tmem_ld16(tl + NT + wlo, w);
 #pragma unroll
-        for (int m = 0; m < NT / 4; m++) {
-          const float4 q4 = __ldcg(reinterpret_cast<const float4*>(rp) + m);
-          pre[4 * m] = q4.x;
-          pre[4 * m + 1] = q4.y;
-          pre[4 * m + 2] = q4.z;
-          pre[4 * m + 3] = q4.w;
-        }
-        if (warp == 2 && lane == 0) sh.counters[t] = 0;
-      }
-      mbar_wait(&acc_full[buf], (seg >> 1) & 1);
-      tc_fence_after();
-      float v[NT];
-      const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
-#pragma unroll
-      for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
-#pragma unroll
-      for (int j = 0; j < NT; j += 16) {  // + lo half of the activation pair
-        float w[16];
-        tmem_ld16(tl + NT + j, w);
-#pragma unroll
-        for (int i = 0; i < 16; i++) v[j + i] += w[i];
-      }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[buf]);
-      if (threadIdx.x == 64) GEMM_PROBE(8 + 2 * (seg & 1));
-      bool run_epi = whole;
-      if (nc == 2) {
-        if (j == 0) {
-#pragma unroll
-          for (int m = 0; m < NT; m++) v[m] += pre[m];   // own + partial 1: contributor order
-          run_epi = true;
-        } else {  // tail contributor: publish (one gpu-scope release) and leave
-          float* wp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
-#pragma unroll
-          for (int m = 0; m < NT; m += 4)
-            __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
-          named_bar_sync(1, 128);
-          if (warp == 2 && lane == 0) {
-            __threadfence();
-            atomicAdd(&sh.counters[t], 1);
+          for (int i = 0; i < EW; i++) v[i] += w[i];
+        };
+        if (threadIdx.x == 64) GEMM_PROBE(8 + 2 * (seg & 1));
+        bool run_epi = whole;
+        if (!whole) {
+          // the head of a two-contributor tile waits for the tail's partial
+          // (published at the start of the tail's run); otherwise the last
+          // contributor to arrive finishes the tile
+          bool publish = !(nc == 2 && j == 0);
+          if (publish && nc > 2) {
+            if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
+            named_bar_sync(1, 128);
+            publish = *s_flag != 2;
           }
-        }
-      } else if (!whole) {
-        // every other contributor already published (the common case for the CTA
-        // finishing a tile last): reduce from registers, no partial round trip
-        if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
-        named_bar_sync(1, 128);
-        const bool fast = *s_flag == 2;
-        if (!fast) {
-          float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
+          if (publish) {
+            float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
+            for (int wlo = 0; wlo < NT; wlo += EW) {
+              float v[EW];
+              own_window(wlo, v);
 #pragma unroll
-          for (int m = 0; m < NT; m += 4)
-            __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
-          // one gpu-scope release by the counting thread: bar.sync orders the other
-          // threads' partial stores before it (fence cumulativity)
-          named_bar_sync(1, 128);
-          if (warp == 2 && lane == 0) {
-            __threadfence();
-            const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
-            if (last) __threadfence();   // acquire: every contributor's partial is visible
-            *s_flag = last;
+              for (int m = 0; m < EW; m += 4)
+                __stcg(reinterpret_cast<float4*>(wp + wlo + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+            }
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) {
+              __threadfence();
+              const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+              if (last) __threadfence();   // acquire: every contributor's partial is visible
+              *s_flag = last;
+            }
+            named_bar_sync(1, 128);
+            run_epi = nc > 2 && *s_flag;
+          } else {
+            run_epi = true;
           }
-          named_bar_sync(1, 128);
-          run_epi = *s_flag;
-        } else {
-          run_epi = true;
+          if (run_epi && nc == 2) {   // head: the tail's partial is published (or about to be)
+            if (warp == 2 && lane == 0)
+              while (ld_acquire_gpu(&sh.counters[t]) < 1) __nanosleep(64);
+            named_bar_sync(1, 128);
+          }
         }
         if (run_epi) {
-          float own[NT];
+          for (int wlo = 0; wlo < NT; wlo += EW) {
+            if (wlo > 0) epi_prefetch<NT, EW, true>(sh, ep, t, row, wlo, wlo + EW, true, pw);
+            float v[EW];
+            if (whole) {
+              own_window(wlo, v);
+            } else {
 #pragma unroll
-          for (int m = 0; m < NT; m++) {
-            own[m] = v[m];
-            v[m] = 0.f;
-          }
-          // partials summed in contributor order (deterministic, whichever CTA is
-          // last); loads of up to four contributors are in flight together
-          for (int j0 = 0; j0 < nc; j0 += 4) {
-            float4 pv[4][NT / 4];
+              for (int m = 0; m < EW; m++) v[m] = 0.f;
+              for (int jj = 0; jj < nc; jj++) {   // contributor order (deterministic)
+                float x[EW];
+                if (jj == j) {
+                  own_window(wlo, x);
+                } else {
+                  const float* rp = sh.ws + (((size_t)t * sh.max_contrib + jj) * 128 + row) * NT + wlo;
 #pragma unroll
-            for (int jj = 0; jj < 4; jj++) {
-              if (j0 + jj < nc && j0 + jj != j) {
-                const float* rp = sh.ws + (((size_t)t * sh.max_contrib + j0 + jj) * 128 + row) * NT;
+                  for (int m = 0; m < EW / 4; m++) {
+                    const float4 q4 = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+                    x[4 * m] = q4.x;
+                    x[4 * m + 1] = q4.y;
+                    x[4 * m + 2] = q4.z;
+                    x[4 * m + 3] = q4.w;
+                  }
+                }
 #pragma unroll
-                for (int m = 0; m < NT / 4; m++) pv[jj][m] = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+                for (int m = 0; m < EW; m++) v[m] += x[m];
               }
             }
+            if (ep.scale_ssq) {
 #pragma unroll
-            for (int jj = 0; jj < 4; jj++) {
-              if (j0 + jj < nc) {
-                if (j0 + jj == j) {
-#pragma unroll
-                  for (int m = 0; m < NT; m++) v[m] += own[m];
-                } else {
-#pragma unroll
-                  for (int m = 0; m < NT / 4; m++) {
-                    v[4 * m] += pv[jj][m].x;
-                    v[4 * m + 1] += pv[jj][m].y;
-                    v[4 * m + 2] += pv[jj][m].z;
-                    v[4 * m + 3] += pv[jj][m].w;
+              for (int m = 0; m < EW; m++) v[m] *= s_inv[wlo + m];
+            }
+            gemm_epilogue<NT, EW, true>(sh, ep, t, row, v, xch, stop, wlo, wlo + EW, pw);
+          }
+          if (!whole && warp == 2 && lane == 0) sh.counters[t] = 0;
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+        if (threadIdx.x == 64) GEMM_PROBE(12 + (seg & 1));
+      } else {
+        float pre[NT];
+        if (nc == 2 && j == 0) {
+          if (warp == 2 && lane == 0)
+            while (ld_acquire_gpu(&sh.counters[t]) < 1) __nanosleep(64);
+          named_bar_sync(1, 128);
+          const float* rp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
+  #pragma unroll
+          for (int m = 0; m < NT / 4; m++) {
+            const float4 q4 = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+            pre[4 * m] = q4.x;
+            pre[4 * m + 1] = q4.y;
+            pre[4 * m + 2] = q4.z;
+            pre[4 * m + 3] = q4.w;
+          }
+          if (warp == 2 && lane == 0) sh.counters[t] = 0;
+        }
+        mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+        tc_fence_after();
+        float v[NT];
+        const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
+  #pragma unroll
+        for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
+  #pragma unroll
+        for (int j = 0; j < NT; j += 16) {  // + lo half of the activation pair
+          float w[16];
+          tmem_ld16(tl + NT + j, w);
+  #pragma unroll
+          for (int i = 0; i < 16; i++) v[j + i] += w[i];
+        }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[buf]);
+        if (threadIdx.x == 64) GEMM_PROBE(8 + 2 * (seg & 1));
+        bool run_epi = whole;
+        if (nc == 2) {
+          if (j == 0) {
+  #pragma unroll
+            for (int m = 0; m < NT; m++) v[m] += pre[m];   // own + partial 1: contributor order
+            run_epi = true;
+          } else {  // tail contributor: publish (one gpu-scope release) and leave
+            float* wp = sh.ws + (((size_t)t * sh.max_contrib + 1) * 128 + row) * NT;
+  #pragma unroll
+            for (int m = 0; m < NT; m += 4)
+              __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) {
+              __threadfence();
+              atomicAdd(&sh.counters[t], 1);
+            }
+          }
+        } else if (!whole) {
+          // every other contributor already published (the common case for the CTA
+          // finishing a tile last): reduce from registers, no partial round trip
+          if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
+          named_bar_sync(1, 128);
+          const bool fast = *s_flag == 2;
+          if (!fast) {
+            float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
+  #pragma unroll
+            for (int m = 0; m < NT; m += 4)
+              __stcg(reinterpret_cast<float4*>(wp + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
+            // one gpu-scope release by the counting thread: bar.sync orders the other
+            // threads' partial stores before it (fence cumulativity)
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) {
+              __threadfence();
+              const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
+              if (last) __threadfence();   // acquire: every contributor's partial is visible
+              *s_flag = last;
+            }
+            named_bar_sync(1, 128);
+            run_epi = *s_flag;
+          } else {
+            run_epi = true;
+          }
+          if (run_epi) {
+            float own[NT];
+  #pragma unroll
+            for (int m = 0; m < NT; m++) {
+              own[m] = v[m];
+              v[m] = 0.f;
+            }
+            // partials summed in contributor order (deterministic, whichever CTA is
+            // last); loads of up to four contributors are in flight together
+            for (int j0 = 0; j0 < nc; j0 += 4) {
+              float4 pv[4][NT / 4];
+  #pragma unroll
+              for (int jj = 0; jj < 4; jj++) {
+                if (j0 + jj < nc && j0 + jj != j) {
+                  const float* rp = sh.ws + (((size_t)t * sh.max_contrib + j0 + jj) * 128 + row) * NT;
+  #pragma unroll
+                  for (int m = 0; m < NT / 4; m++) pv[jj][m] = __ldcg(reinterpret_cast<const float4*>(rp) + m);
+                }
+              }
+  #pragma unroll
+              for (int jj = 0; jj < 4; jj++) {
+                if (j0 + jj < nc) {
+                  if (j0 + jj == j) {
+  #pragma unroll
+                    for (int m = 0; m < NT; m++) v[m] += own[m];
+                  } else {
+  #pragma unroll
+                    for (int m = 0; m < NT / 4; m++) {
+                      v[4 * m] += pv[jj][m].x;
+                      v[4 * m + 1] += pv[jj][m].y;
+                      v[4 * m + 2] += pv[jj][m].z;
+                      v[4 * m + 3] += pv[jj][m].w;
+                    }
                   }
                 }
               }
             }
+            if (warp == 2 && lane == 0) sh.counters[t] = 0;
           }
-          if (warp == 2 && lane == 0) sh.counters[t] = 0;
+          named_bar_sync(1, 128);
         }
-        named_bar_sync(1, 128);
-      }
-      if (threadIdx.x == 64) GEMM_PROBE(12 + (seg & 1));
-      if (run_epi) {
-        if (ep.scale_ssq) {
-#pragma unroll
-          for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+        if (threadIdx.x == 64) GEMM_PROBE(12 + (seg & 1));
+        if (run_epi) {
+          if (ep.scale_ssq) {
+  #pragma unroll
+            for (int m = 0; m < NT; m++) v[m] *= s_inv[m];
+          }
+          gemm_epilogue<NT, NT, false>(sh, ep, t, row, v, xch, stop, 0, NT, pf);
         }
-        gemm_epilogue<NT, NT, false>(sh, ep, t, row, v, xch, stop, 0, NT, pf);
       }
       if (threadIdx.x == 64) GEMM_PROBE(9 + 2 * (seg & 1));
       u = seg_end;
