@@ -910,17 +910,18 @@ int launch_attention(fs_ctx* c, int l) {
       lc.numAttrs = 1;
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 +
                                            (double)nsplit * Hkv * QR * (hd + 2) * 4 * 2);
-      // P format of P.V: fp16 with V converted to fp16 in shared memory by the softmax
-      // warps (default: one P.V MMA, 72B layer 40.2 us, logits 9.5e-3), the bf16 hi/lo
-      // pair (FS_TC_ATTN_P=hilo: two P.V MMAs, 43.5 us, 9.8e-3) or plain bf16
-      // (FS_TC_ATTN_P=bf16: 38.8 us but 0.027 > 2e-2 on the logits).  f16 P with bf16 V
-      // is not a valid kind::f16 instruction (A and B formats must match); a V outside
+      // P format of P.V: the bf16 hi/lo pair (default: two P.V MMAs, 72B 16K layer
+      // 37.4 us with the warp combine), fp16 with V converted to fp16 in shared memory
+      // by the softmax warps (FS_TC_ATTN_P=f16: one P.V MMA, 3-4 us less per layer, but
+      // the 80-layer 72B logits reach 0.0212 > 2e-2, hi/lo 0.019) or plain bf16
+      // (FS_TC_ATTN_P=bf16: 0.027 > 2e-2 on 2 layers).  f16 P with bf16 V is not a
+      // valid kind::f16 instruction (A and B formats must match); with f16, a V outside
       // fp16's range fails the call with FS_ERANGE
       const char* pfe = getenv("FS_TC_ATTN_P");
       const int pf = getenv("FS_TC_ATTN_P_BF16") ? TCA_P_BF16
-                     : !pfe ? TCA_P_F16
-                     : !strcmp(pfe, "hilo") ? TCA_P_HILO
-                     : !strcmp(pfe, "bf16") ? TCA_P_BF16 : TCA_P_F16;
+                     : !pfe ? TCA_P_HILO
+                     : !strcmp(pfe, "f16") ? TCA_P_F16
+                     : !strcmp(pfe, "bf16") ? TCA_P_BF16 : TCA_P_HILO;
       auto go = [&](auto kern, int threads, int smem_bytes) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         lc.blockDim = dim3(threads);

@@ -84,23 +84,25 @@ def test_72b_gqa_online_softmax_rescale_path(monkeypatch):
     _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
 
 
-def test_72b_gqa_hilo_p_path(monkeypatch):
-    """The bf16 hi/lo P variant of the GQA kernel (two P.V MMAs, bf16 V) stays
-    selectable (FS_TC_ATTN_P=hilo) and parity-green on the configs[4] shapes."""
-    monkeypatch.setenv("FS_TC_ATTN_P", "hilo")
+def test_72b_gqa_f16_p_path(monkeypatch):
+    """The fp16-P variant of the GQA kernel (V converted to fp16 in shared memory
+    by the softmax warps, one P.V MMA; opt-in FS_TC_ATTN_P=f16) is parity-green
+    on the configs[4] per-layer shapes."""
+    monkeypatch.setenv("FS_TC_ATTN_P", "f16")
     _run("72b_l2", 16384, "synth", 32, 32, 256, 8, (0, 3, 9, 40, 47, 70, 90, 100, 120), 17408, 1)
 
 
 @pytest.mark.parametrize("name,seg,env,fails", [
-    ("72b_l2", 32, {}, True),                          # GQA tcgen05 kernel, fp16 P (default)
-    ("72b_l2", 32, {"FS_TC_ATTN_P": "hilo"}, False),   # GQA, bf16 hi/lo P: reads bf16 V directly
+    ("72b_l2", 32, {"FS_TC_ATTN_P": "f16"}, True),     # GQA tcgen05 kernel, fp16 P (opt-in)
+    ("72b_l2", 32, {}, False),                         # GQA, bf16 hi/lo P (default): reads bf16 V directly
     ("7b_l2", 16, {}, True),                           # MHA cluster kernel, fp16 P.V fragments
     ("7b_l2", 16, {"FS_MHA_TMA": "1"}, True),          # MHA TMA-ring kernel
 ])
 def test_fp16_pv_v_range_fails_loudly(monkeypatch, name, seg, env, fails):
-    """The fp16 P.V paths convert V (bf16) to fp16 on chip: a V row outside
-    fp16's range (|v| >= 65536) must fail the verify step with FS_ERANGE (and
-    poison the context), never produce a silent inf; the GQA hi/lo variant
+    """The fp16 P.V paths (the MHA kernels; the GQA kernel with
+    FS_TC_ATTN_P=f16) convert V (bf16) to fp16 on chip: a V row outside fp16's
+    range (|v| >= 65536) must fail the verify step with FS_ERANGE (and poison
+    the context), never produce a silent inf; the default GQA hi/lo variant
     reads bf16 V directly and accepts the same row."""
     import torch
     if not torch.cuda.is_available():

@@ -23,6 +23,9 @@ def _full(name, prefix_len, n_nodes, depth, l_max, max_seg, planted, n_segments,
         pytest.skip("no GPU")
     from paper_2507_02620_b200 import flowspec as F
     shape = SHAPES[name]
+    import gc
+    gc.collect()                 # pipelines of earlier tests in this process
+    torch.cuda.empty_cache()     # return their cached arenas to the device
     free, _ = torch.cuda.mem_get_info()
     need = shape.n_params * 2 * 1.06
     if free < need:
