@@ -805,7 +805,7 @@ int launch_attention(fs_ctx* c, int l) {
         int ns = std::max(1, occ * c->n_sms / Hkv);
         ns = std::min(ns, (f.max_ctx + ATT_SUB - 1) / ATT_SUB);   // at least one sub-chunk of keys each
         ns = std::min(ns, c->att_chunk_cap * 4);                   // workspace capacity
-        ns = std::min(ns, 8);   // the combine loads 8 splits per round trip (9 splits: 11.4 vs 10.0 us, 7B)
+        ns = std::min(ns, getenv("FS_MHA_NSPLIT_CAP") ? atoi(getenv("FS_MHA_NSPLIT_CAP")) : 8);
         if (getenv("FS_ATT_NSPLIT")) ns = std::max(1, std::min(ns, atoi(getenv("FS_ATT_NSPLIT"))));
         c->mha_nsplit[MT] = ns;
       }

@@ -487,12 +487,16 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
         for (int i = 0; i < 8; i++) {
           const int k0 = c16 * 16 + 2 * i;
           const float x0 = ex2_approx(fmaf(sv[k0], sc, nm)), x1 = ex2_approx(fmaf(sv[k0 + 1], sc, nm));
-          ls[i & 3] += x0 + x1;
           uint32_t u;
           if constexpr (PF == TCA_P_F16) {
+            // the row sum takes the fp16-rounded weights the P.V MMA uses, so O / l
+            // is an exact weighted mean of V (consistent normalisation)
             const __half2 hv = __floats2half2_rn(x0, x1);
+            const float2 hr = __half22float2(hv);
+            ls[i & 3] += hr.x + hr.y;
             u = *reinterpret_cast<const uint32_t*>(&hv);
           } else {
+            ls[i & 3] += x0 + x1;
             const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
             u = *reinterpret_cast<const uint32_t*>(&hb);
           }
