@@ -189,6 +189,9 @@ struct fs_ctx {
   int q_rows = 0;
   // profiling: event pairs around GEMM / attention launches
   bool prof = false;
+  // FS_XCHG_TIMING (diagnostics): CUDA-event pairs around every NCCL tick exchange and
+  // every stage forward, summarised to stderr at fs_destroy
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> xt_x, xt_f;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, double>> ev_used;  // (kind 0 gemm / 1 attn, bytes) per pair
   size_t ev_next = 0;
@@ -1182,11 +1185,22 @@ int exchange(fs_ctx* c, const void* sptr, size_t sw, void* rptr, size_t rw, void
   const int p = c->rank, P = c->P;
   if (P == 1 || (!sw && !rw && !bw)) return FS_OK;
   if (!c->lg) {
+    static const bool xt = getenv("FS_XCHG_TIMING") != nullptr;
+    cudaEvent_t xa = nullptr, xb = nullptr;
+    if (xt) {
+      cudaEventCreate(&xa);
+      cudaEventCreate(&xb);
+      cudaEventRecord(xa, c->st);
+    }
     CK_NCCL(c, ncclGroupStart());
     if (sw) CK_NCCL(c, ncclSend(sptr, sw, ncclFloat32, p + 1, c->comm, c->st));
     if (rw) CK_NCCL(c, ncclRecv(rptr, rw, ncclFloat32, p - 1, c->comm, c->st));
     if (bw) CK_NCCL(c, ncclBroadcast(bptr, bptr, bw, ncclInt32, P - 1, c->comm, c->st));
     CK_NCCL(c, ncclGroupEnd());
+    if (xt) {
+      cudaEventRecord(xb, c->st);
+      c->xt_x.push_back({xa, xb});
+    }
     return FS_OK;
   }
   fs_local_group* g = c->lg;
@@ -2482,6 +2496,20 @@ void fs_local_group_destroy(fs_local_group* g) { delete g; }
 void fs_destroy(fs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
+  if (!c->xt_x.empty()) {
+    cudaDeviceSynchronize();
+    std::vector<double> d;
+    for (auto& e : c->xt_x) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e.first, e.second);
+      d.push_back(1e3 * ms);
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    std::sort(d.begin(), d.end());
+    fprintf(stderr, "[rank %d] NCCL tick exchanges: %zu, min %.1f us, median %.1f us, p90 %.1f us\n", c->rank,
+            d.size(), d[0], d[d.size() / 2], d[d.size() * 9 / 10]);
+  }
   if (c->lg) {
     std::lock_guard<std::mutex> lk(c->lg->mu);
     if (c->lg->member[c->rank] == c) c->lg->member[c->rank] = nullptr;
