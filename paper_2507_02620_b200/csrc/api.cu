@@ -109,7 +109,7 @@ struct fs_ctx {
   bool wide = false;                // the prefill-chunk width is active
   int att_dbg_ends = 0;
   int att_nsplit[3] = {0, 0, 0};   // MHA attention key splits per m-tile count (planned once)
-  int mha_nsplit[3] = {0, 0, 0};   // TMA MHA attention: splits per m-tile count (SM-count sized)
+  int mha_nsplit[5] = {0, 0, 0, 0, 0};   // TMA MHA attention: splits per m-tile count (SM-count sized)
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
   fs_local_group* lg = nullptr;           // single-process stage transport (else NCCL)
@@ -786,20 +786,23 @@ int launch_attention(fs_ctx* c, int l) {
     const bool mha_tma = getenv("FS_MHA_CP_ASYNC") ? false
                          : getenv("FS_MHA_TMA") ? true
                          : n_keys > MHA_TMA_MIN_KEYS;
-    if (MT <= 2 && hd == ATT_HD && mha_tma) {
+    // prefill chunks of an MHA model (64 query rows, MT 4) also take the TMA kernel
+    if ((MT <= 2 && hd == ATT_HD && mha_tma) || (MT == 4 && hd == ATT_HD && !getenv("FS_MHA_CP_ASYNC"))) {
       // MHA path: TMA-staged K/V ring, splits sized to fill every SM slot,
       // partials merged by attn_combine_kernel (programmatic launch)
-      const size_t smem = mha_tma_smem(np, c->ancw);
+      const size_t smem = mha_tma_smem(np, c->ancw, QR);
       static std::atomic<uint64_t> tattr{0};
-      once_per_device(tattr, c, [] {   // the largest any context needs (npad 64, max_live 512)
-        const int mx = (int)mha_tma_smem(64, FS_MAX_LIVE / 32);
+      once_per_device(tattr, c, [] {   // the largest any context needs (npad 64, max_live 512, QR 64)
+        const int mx = (int)mha_tma_smem(64, FS_MAX_LIVE / 32, 64);
         cudaFuncSetAttribute(attn_mha_tma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(attn_mha_tma_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(attn_mha_tma_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
       });
       if (c->mha_nsplit[MT] == 0) {
         int occ = 0;
-        if ((MT == 1 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<16>, MHA_THREADS, smem)
-                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<32>, MHA_THREADS, smem)) !=
+        if ((MT == 1   ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<16>, MHA_THREADS, smem)
+             : MT == 2 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<32>, MHA_THREADS, smem)
+                       : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, attn_mha_tma_kernel<64>, MHA_THREADS, smem)) !=
                 cudaSuccess ||
             occ < 1) {
           cudaGetLastError();
@@ -826,8 +829,10 @@ int launch_attention(fs_ctx* c, int l) {
       const int api = prof_begin(c, 1, (double)n_keys * Hkv * hd * 2 * 2 + (double)QR * Hkv * hd * 2 * 3);
       if (MT == 1)
         cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<16>, c->lw[l].mk, c->lw[l].mv, a);
-      else
+      else if (MT == 2)
         cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<32>, c->lw[l].mk, c->lw[l].mv, a);
+      else
+        cudaLaunchKernelEx(&lc, attn_mha_tma_kernel<64>, c->lw[l].mk, c->lw[l].mv, a);
       CK_LAUNCH(c);
       launch_combine(c, a, at, nsplit);
       prof_end(c, api);

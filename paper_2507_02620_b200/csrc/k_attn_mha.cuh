@@ -30,9 +30,10 @@ constexpr int MHA_BOX = ATT_SUB * 128;             // one [64 keys][64 dims] bf1
 constexpr int MHA_STAGE = 4 * MHA_BOX;             // K (2 boxes) | V (2 boxes) = 32 KB
 constexpr int MHA_THREADS = 160;                   // 4 consumer warps + 1 TMA warp
 constexpr int MHA_TMA_MIN_KEYS = 2048;             // shorter contexts: the cluster kernel
-// dynamic smem: ring | Q [32][LD] | anc [npad][ancw] | barriers
-__host__ __device__ constexpr size_t mha_tma_smem(int npad, int ancw) {
-  return 1024 + (size_t)MHA_NST * MHA_STAGE + (size_t)ATT_MAXQR * ATT_LD * 2 + (size_t)npad * ancw * 4 + 256;
+// dynamic smem: ring | Q [QR][LD] | anc [npad][ancw] | barriers  (QR = G * npad
+// query rows: 16 / 32 for tree segments, 64 for prefill chunks)
+__host__ __device__ constexpr size_t mha_tma_smem(int npad, int ancw, int qr) {
+  return 1024 + (size_t)MHA_NST * MHA_STAGE + (size_t)qr * ATT_LD * 2 + (size_t)npad * ancw * 4 + 256;
 }
 
 
@@ -44,7 +45,8 @@ __global__ void __launch_bounds__(MHA_THREADS) attn_mha_tma_kernel(const __grid_
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(att_smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sRing = smem;
   bf16* sQ = reinterpret_cast<bf16*>(sRing + (size_t)MHA_NST * MHA_STAGE);
-  uint32_t* sAnc = reinterpret_cast<uint32_t*>(sQ + (size_t)ATT_MAXQR * ATT_LD);
+  const int QRs = (a.H / a.Hkv) * a.npad;
+  uint32_t* sAnc = reinterpret_cast<uint32_t*>(sQ + (size_t)QRs * ATT_LD);
   uint64_t* full = reinterpret_cast<uint64_t*>(sAnc + (size_t)a.npad * a.ancw);
   uint64_t* empty = full + MHA_NST;
   int* sCtxMin = reinterpret_cast<int*>(empty + MHA_NST);
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(MHA_THREADS) attn_mha_tma_kernel(const __grid_
   // ---- merge the key-warps of each m-tile (the ring is free: every stage consumed)
   float* so = reinterpret_cast<float*>(sRing);
   float* sPart = so + 4 * 16 * ATT_SO_LD + 4 * 16 * 2;
-  float* sPml = sPart + ATT_MAXQR * ATT_HD;
+  float* sPml = sPart + QRs * ATT_HD;   // so | sml | sPart | sPml fit the free ring (<= 68 KB at QR 64)
   mha_ks_merge<KPW>(w, a, so, sPart, sPml, tid, warp, lane, 1);
   named_bar_sync(1, 128);
   // ---- this split's partial -> workspace [split][Hkv][QR][HD] (+ [..][2]), coalesced
