@@ -20,6 +20,7 @@ through the same public API; untimed dry runs check that tree verification
 commits the plan.  Weights >> L2 (126 MB): every tick streams them from HBM.
 """
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -36,7 +37,7 @@ SEED = 0x5EED01
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
@@ -435,6 +436,10 @@ def ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = gp.state()["launches"]
+    # host hygiene for both timed regions (as timeit does): no cyclic-GC pause
+    # inside them; the library allocates nothing per call on the host side
+    gc.collect()
+    gc.disable()
     clocks.t_from = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
@@ -474,6 +479,7 @@ def ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         wall = float(tt.item())
     e2e = e_tokens / wall
+    gc.enable()
     if S:
         sr.end()
     # keep the same load (one-node verify rounds) until the sampler has seen
@@ -590,6 +596,7 @@ def ours(args):
             "scaling_note": "the same workload at every N (strong scaling: fixed work, P splits the "
                             "layer stack)",
             "l2": "inputs larger than L2: the weights stream from HBM every tick",
+            "host": "Python cyclic GC disabled inside the timed regions (as timeit does)",
             "tokens_per_step": tokens / K,
             "ticks_per_step": ticks / K,
             "planted_stream": plan_info,
