@@ -432,14 +432,15 @@ def ours(args):
 
     for r in range(W):
         step(r)
+    # host hygiene for both timed regions (as timeit does): no cyclic-GC pause
+    # inside them (collected before the barrier, so no rank enters the timed
+    # region late and makes its peers wait inside it)
+    gc.collect()
+    gc.disable()
+    launches0 = gp.state()["launches"]
     if P > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = gp.state()["launches"]
-    # host hygiene for both timed regions (as timeit does): no cyclic-GC pause
-    # inside them; the library allocates nothing per call on the host side
-    gc.collect()
-    gc.disable()
     clocks.t_from = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)

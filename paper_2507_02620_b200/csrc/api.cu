@@ -1123,7 +1123,7 @@ int stage_forward(fs_ctx* c, bool from_hin) {
   if (c->bf) {  // embedding / received rows -> x, and the first RMSNorm's inputs (one kernel)
     const bf16* g0 = c->nl > 0 ? (const bf16*)c->lw[0].g1 : (const bf16*)c->gf;
     const float* src = (!c->first && from_hin) ? c->hin : c->x;
-    norm_prep_kernel<bf16><<<c->npad, 128, 0, c->st>>>(c->first ? (const bf16*)c->emb : nullptr, src, c->x,
+    norm_prep_kernel<bf16><<<dim3(c->npad, std::max(1, d / 512)), 128, 0, c->st>>>(c->first ? (const bf16*)c->emb : nullptr, src, c->x,
                                                        g0, (bf16*)c->y, c->ssq, d, c->d_rows);
     CK_LAUNCH(c);
   } else if (c->first) {

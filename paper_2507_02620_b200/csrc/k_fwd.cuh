@@ -23,21 +23,25 @@ __global__ void embed_kernel(const T* __restrict__ E, int d, const TickRows* row
 // First RMSNorm input of a stage's forward: x = the embedding rows (E != null),
 // the received rows (src != x) or x as it is; then per-32-column sums of
 // squares of x [d/32][npad] and z = x*g as the bf16 hi/lo B operand [2*npad][d]
-// (RMSNorm applied by linearity in the GEMM).  Warp w of the CTA covers the
-// 32-column groups 4i + w with coalesced loads; rows >= n_rows give z = 0.
+// (RMSNorm applied by linearity in the GEMM).  CTA (m, y) covers the 32-column
+// groups g = 4 * (y + gridDim.y * i) + w (warp w) with coalesced loads, so a row
+// is spread over gridDim.y CTAs (latency: every load of a row in flight);
+// rows >= n_rows give z = 0.
 template <typename TE>
 __global__ void __launch_bounds__(128) norm_prep_kernel(const TE* __restrict__ E, const float* src, float* x,
                                                         const bf16* __restrict__ g, bf16* z, float* ssq, int d,
                                                         const TickRows* rows) {
   const int m = blockIdx.x, np = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cy = blockIdx.y, ny = gridDim.y;
   const bool live = m < rows->n_rows;
   const TE* er = (E && live) ? E + (size_t)rows->token[m] * d : nullptr;
   const float* xs = (E ? x : src) + (size_t)m * d;
   float* xr = x + (size_t)m * d;
   const int ng = d / 32;   // d % 32 == 0 (cfg_valid): whole groups, warp-uniform bound
-#pragma unroll 4
-  for (int i = 0; i * 4 + warp < ng; i++) {
-    const int k = i * 128 + warp * 32 + lane;
+#pragma unroll 2
+  for (int i = 0; (cy + ny * i) * 4 + warp < ng; i++) {
+    const int grp = (cy + ny * i) * 4 + warp;
+    const int k = grp * 32 + lane;
     float v = 0.f;
     if (live) {
       v = er ? to_f32(er[k]) : xs[k];
@@ -50,7 +54,7 @@ __global__ void __launch_bounds__(128) norm_prep_kernel(const TE* __restrict__ E
     float s = v * v;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) ssq[(size_t)(i * 4 + warp) * np + m] = s;
+    if (lane == 0) ssq[(size_t)grp * np + m] = s;
   }
 }
 
