@@ -131,3 +131,12 @@ def test_fp16_pv_v_range_fails_loudly(monkeypatch, name, seg, env, fails):
     with pytest.raises(F.FlowSpecError) as e:
         gp.fs_verify_step()
     assert e.value.code == F.FS_EPOISONED
+
+
+def test_gqa_many_splits_combine_batches():
+    """smallq (GQA 8/2) with 32-row segments runs the tcgen05 GQA kernel with
+    one split per 2 SMs of a kv head, capped by the workspace: at max_ctx 2048
+    that is 64 splits, so the warp combine merges two 32-split batches (the
+    running maximum raised between batches) and most splits are empty (neutral
+    partials).  Lockstep with the oracle."""
+    _run("smallq", 1400, "synth", 32, 32, 96, 6, (0, 2, 5, 17, 21, 40), 2048, 2)
