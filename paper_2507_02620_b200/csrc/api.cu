@@ -1119,7 +1119,6 @@ int head_forward(fs_ctx* c) {
 // this stage's forward of the rows in d_rows (h_rows mirrors it on the host)
 int stage_forward(fs_ctx* c, bool from_hin) {
   const int d = c->cfg.d_model;
-  const int n = c->h_rows->n_rows;
   if (c->bf) {  // embedding / received rows -> x, and the first RMSNorm's inputs (one kernel)
     const bf16* g0 = c->nl > 0 ? (const bf16*)c->lw[0].g1 : (const bf16*)c->gf;
     const float* src = (!c->first && from_hin) ? c->hin : c->x;

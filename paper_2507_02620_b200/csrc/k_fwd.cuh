@@ -910,8 +910,6 @@ __global__ void __launch_bounds__(128) attn_mha_kernel(AttnMhaArgs args) {
   const TickRows* rows = a.rows;
   const int G = a.H / a.Hkv;
   const int QR = G * a.npad;
-  const int MT = QR / 16;
-  constexpr int KS = ATT_SUB / KPW;
   // smem: Q [QR][LD] | K/V ring [NBUF][K|V][SUB][LD] | ancestor rows [npad][ancw]
   // after the key loop the ring is reused: key-warp states [4][16][HD] + [4][16][2],
   // then the CTA partial [QR][HD] + [QR][2] read by the cluster peers

@@ -624,13 +624,13 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
         float v[NT];
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
   #pragma unroll
-        for (int j = 0; j < NT; j += 16) tmem_ld16(tl + j, v + j);
+        for (int jc = 0; jc < NT; jc += 16) tmem_ld16(tl + jc, v + jc);
   #pragma unroll
-        for (int j = 0; j < NT; j += 16) {  // + lo half of the activation pair
+        for (int jc = 0; jc < NT; jc += 16) {  // + lo half of the activation pair
           float w[16];
-          tmem_ld16(tl + NT + j, w);
+          tmem_ld16(tl + NT + jc, w);
   #pragma unroll
-          for (int i = 0; i < 16; i++) v[j + i] += w[i];
+          for (int i = 0; i < 16; i++) v[jc + i] += w[i];
         }
         tc_fence_before();
         mbar_arrive(&acc_empty[buf]);

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(SWT) sample_walk_cluster_kernel(SampleArgs a) 
       double loc = 0.0;
       for (int i = b0; i < b1; i++) loc += r[i];
       // slice total (block sum) published in slot[2]
-      double tot = loc, tdum = 0.0;
+      double tot = loc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
       __syncthreads();
@@ -407,7 +407,6 @@ __global__ void __launch_bounds__(SWT) sample_walk_cluster_kernel(SampleArgs a) 
         slot[5] = 1e300;   // this CTA's sample margin (set by the owner only)
         s_pick = -1;
       }
-      (void)tdum;
       cluster_sync_acqrel();
       double before = 0.0, total = 0.0;
       if (tid == 0) {
