@@ -635,7 +635,7 @@ int launch_gemm_nt(fs_ctx* c, const GemmOp& g, const GemmEpi& ep) {
     }
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(g.sh.n_tiles * g.split);
-    lc.blockDim = dim3(GemmCfg<NT>::THREADS);
+    lc.blockDim = dim3(192);   // gemm_cluster_kernel: TMA, MMA, 4 epilogue warps at every width
     lc.dynamicSmemBytes = GemmCfg<NT>::SMEM;
     lc.stream = c->st;
     cudaLaunchAttribute at[2];

@@ -122,7 +122,10 @@ struct GemmCfg {
   static constexpr int TOP_BYTES = 4 * NT * (int)sizeof(Top2);
   static constexpr int INV_BYTES = 64 * 4;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256 + XCH_BYTES + TOP_BYTES + INV_BYTES;
-  static constexpr int THREADS = 192;   // TMA producer, MMA issuer, 4 epilogue warps
+  // TMA producer, MMA issuer, 4 epilogue warps (8 at NT 64: two groups of 4,
+  // each finishing half of the 16-column windows of a prefill-width tile)
+  static constexpr int EPW = NT > 32 ? 8 : 4;
+  static constexpr int THREADS = 64 + 32 * EPW;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
@@ -208,7 +211,7 @@ FS_DEV float warp_colsum(const float* v, int lane, int& col) {
 // W = NT / S window for cluster split-K rank r).
 template <int NT, int W, bool PFR = true>
 FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row, float* v,
-                          float* xch, Top2* stop, int mlo, int mhi, const EpiPre<W>& p) {
+                          float* xch, Top2* stop, int mlo, int mhi, const EpiPre<W>& p, int bar = 1) {
   const TickRows* rows = ep.rows;
   const int n_rows = p.n_rows;
   constexpr bool PF = PFR && W <= 16;   // per-row operands prefetched
@@ -226,7 +229,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
     if (hh < H + Hkv) {  // rotate-half RoPE on q and k heads (partner row ^ 64)
 #pragma unroll
       for (int j = 0; j < W; j++) xch[row * (W + 1) + j] = v[j];
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
       const int i = row & 63;
 #pragma unroll
       for (int j = 0; j < W; j++) {
@@ -236,7 +239,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
           v[j] = (row < 64) ? (v[j] * cs.x - pv * cs.y) : (v[j] * cs.x + pv * cs.y);
         }
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
     }
 #pragma unroll
     for (int j = 0; j < W; j++) {
@@ -256,7 +259,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
   } else if (ep.mode == EPI_GLU) {
 #pragma unroll
     for (int j = 0; j < W; j++) xch[row * (W + 1) + j] = v[j];
-    named_bar_sync(1, 128);
+    named_bar_sync(bar, 128);
     if (row < 64) {
 #pragma unroll
       for (int j = 0; j < W; j++) {
@@ -269,7 +272,7 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
         ep.act[(size_t)(NT + m) * ep.ffn + t * 64 + row] = __float2bfloat16_rn(a - __bfloat162float(hi));
       }
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(bar, 128);
   } else if (ep.mode == EPI_RESID) {
     float sq[W], xn[W];
     // old residual values first (all loads in flight), then the update
@@ -335,13 +338,13 @@ FS_DEV void gemm_epilogue(const GemmShape& sh, const GemmEpi& ep, int t, int row
       tt = top2_warp(tt);
       if (lane == 0) stop[q * W + j] = tt;
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(bar, 128);
     if (row < jhi) {
       Top2 r = stop[row];
       for (int w = 1; w < 4; w++) r = top2_merge(r, stop[w * W + row]);
       ep.head_part[(size_t)t * NT + mlo + row] = r;
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(bar, 128);
   } else {  // EPI_STORE
     if (ng < sh.n_out)
 #pragma unroll
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     }
     for (int b = 0; b < 2; b++) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 128);
+      mbar_init(&acc_empty[b], 32 * C::EPW);
     }
     fence_barrier_init();
   }
@@ -471,9 +474,12 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
+    // ---------------- epilogue warps 2.. (TMEM lane quarter = warp % 4; group
+    // grp of 4 warps at NT 64)
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    const int grp = (warp - 2) >> 2;
+    constexpr int EPT = 32 * C::EPW;   // epilogue threads
     // previous kernels complete (their outputs are this epilogue's inputs, and
     // their reads of this epilogue's outputs are done); then prefetch
     pdl_wait();
@@ -481,12 +487,12 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
     epi_prefetch<NT, NT, false>(sh, ep, 0, row, 0, NT, false, pf);
     if (ep.scale_ssq) {
       // inv[m] of the RMSNorm applied by linearity (rows >= n_rows: padding)
-      if (row < NT) {
+      if (row < NT && grp == 0) {
         float ss = 0.f;
         for (int i = 0; i < ep.scale_n; i++) ss += ep.scale_ssq[(size_t)i * NT + row];
         s_inv[row] = 1.0f / sqrtf(ss / (float)sh.K + ep.eps);
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, EPT);
     }
     int seg = 0, u = u0;
     while (u < u1) {
@@ -513,7 +519,8 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
         // window 0, loaded while the mainloop still streams; later windows load
         // theirs (all 16 columns in flight) just before use
         EpiPre<EW> pw;
-        epi_prefetch<NT, EW, true>(sh, ep, t, row, 0, EW, true, pw);
+        const int wbeg = grp * (NT / 2), wend = (grp + 1) * (NT / 2);   // this group's windows
+        epi_prefetch<NT, EW, true>(sh, ep, t, row, wbeg, wbeg + EW, true, pw);
         mbar_wait(&acc_full[buf], (seg >> 1) & 1);
         tc_fence_after();
         const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * C::BN);
@@ -533,26 +540,26 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
           bool publish = !(nc == 2 && j == 0);
           if (publish && nc > 2) {
             if (warp == 2 && lane == 0) *s_flag = (ld_acquire_gpu(&sh.counters[t]) == nc - 1) ? 2 : 0;
-            named_bar_sync(1, 128);
+            named_bar_sync(1, EPT);
             publish = *s_flag != 2;
           }
           if (publish) {
             float* wp = sh.ws + (((size_t)t * sh.max_contrib + j) * 128 + row) * NT;
-            for (int wlo = 0; wlo < NT; wlo += EW) {
+            for (int wlo = grp * (NT / 2); wlo < (grp + 1) * (NT / 2); wlo += EW) {   // this group's half
               float v[EW];
               own_window(wlo, v);
 #pragma unroll
               for (int m = 0; m < EW; m += 4)
                 __stcg(reinterpret_cast<float4*>(wp + wlo + m), make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]));
             }
-            named_bar_sync(1, 128);
+            named_bar_sync(1, EPT);
             if (warp == 2 && lane == 0) {
               __threadfence();
               const int last = (atomicAdd(&sh.counters[t], 1) == nc - 1);
               if (last) __threadfence();   // acquire: every contributor's partial is visible
               *s_flag = last;
             }
-            named_bar_sync(1, 128);
+            named_bar_sync(1, EPT);
             run_epi = nc > 2 && *s_flag;
           } else {
             run_epi = true;
@@ -560,12 +567,12 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
           if (run_epi && nc == 2) {   // head: the tail's partial is published (or about to be)
             if (warp == 2 && lane == 0)
               while (ld_acquire_gpu(&sh.counters[t]) < 1) __nanosleep(64);
-            named_bar_sync(1, 128);
+            named_bar_sync(1, EPT);
           }
         }
         if (run_epi) {
-          for (int wlo = 0; wlo < NT; wlo += EW) {
-            if (wlo > 0) epi_prefetch<NT, EW, true>(sh, ep, t, row, wlo, wlo + EW, true, pw);
+          for (int wlo = wbeg; wlo < wend; wlo += EW) {
+            if (wlo > wbeg) epi_prefetch<NT, EW, true>(sh, ep, t, row, wlo, wlo + EW, true, pw);
             float v[EW];
             if (whole) {
               own_window(wlo, v);
@@ -595,7 +602,8 @@ __global__ void __launch_bounds__(GemmCfg<NT>::THREADS, GemmCfg<NT>::MIN_CTAS)
 #pragma unroll
               for (int m = 0; m < EW; m++) v[m] *= s_inv[wlo + m];
             }
-            gemm_epilogue<NT, EW, true>(sh, ep, t, row, v, xch, stop, wlo, wlo + EW, pw);
+            gemm_epilogue<NT, EW, true>(sh, ep, t, row, v, xch + grp * 128 * (EW + 1), stop + grp * 4 * EW, wlo,
+                                        wlo + EW, pw, 2 + grp);
           }
           if (!whole && warp == 2 && lane == 0) sh.counters[t] = 0;
         }
