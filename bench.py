@@ -174,14 +174,15 @@ class Clocks:
 PRUNES = [0]   # fs_prune_and_compact calls (host -> device decision copies)
 
 # bytes the library copies per call (include/flowspec.h capacities: FS_MAX_LIVE
-# 512, FS_MAX_SEG 64): SubmitIn (5 ints + parent / token / own [512]) host ->
-# device per submit; the submit record prefix (11 ints + order [512]) back;
-# the verify step's record (11 ints, 5 x [512] arrays, prune plan 1 + [512],
-# 64 row results of 8 B and 64 node ids) back per tick; DecisionIn (4 ints +
-# acc ids [512]) host -> device per prune
+# 512, FS_MAX_SEG 64; csrc/state.cuh layouts): SubmitIn (5 ints + parent / token
+# / own [512]) host -> device per submit; a synchronous submit reads the record
+# prefix back (14 ints + order / merged [512]), an FS_SUBMIT_ASYNC one (every
+# submit in the timed steps) nothing; the verify step's whole record (14 ints,
+# 6 x [512] arrays, prune plan 1 + [512], 64 row results of 8 B and 64 node ids)
+# back per tick; DecisionIn (4 ints + acc ids [512]) host -> device per prune
 H2D_SUBMIT = 4 * (5 + 3 * 512)
-D2H_SUBMIT = 4 * (11 + 512)
-D2H_TICK = 4 * (11 + 5 * 512 + 1 + 512) + 64 * 8 + 64 * 4
+D2H_SUBMIT = 0   # async submits in the timed steps (a synchronous one: 4 * (14 + 2 * 512))
+D2H_TICK = 4 * (14 + 6 * 512 + 1 + 512) + 64 * 8 + 64 * 4   # sizeof(TreeRecord) = 15164
 H2D_PRUNE = 4 * (4 + 512)
 
 

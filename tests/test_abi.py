@@ -120,3 +120,27 @@ def test_layer_partition_byte_balanced(fsmod):
             assert max(load) - min(load) <= layer + head
     l72 = fsmod.layers_per_stage(SHAPES["72b"], 8)
     assert l72[-1] == min(l72)
+
+
+def test_bench_copy_byte_counts_match_the_library_structs(tmp_path):
+    """bench.py's e2e h2d / d2h byte counts are the library's own copies: the
+    verify-step record, the submit input and the prune decision (internal
+    structs of csrc/state.cuh, measured here with the host compiler)."""
+    import shutil
+    import subprocess
+    import bench
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    src = tmp_path / "sz.cu"
+    src.write_text('#include <cstdio>\n#include <cstddef>\n#include "flowspec.h"\n#include "state.cuh"\n'
+                   'int main() { printf("%zu %zu %zu %zu\\n", sizeof(fs::TreeRecord), '
+                   'offsetof(fs::TreeRecord, acc_s), sizeof(fs::SubmitIn), sizeof(fs::DecisionIn)); }\n')
+    exe = tmp_path / "sz"
+    csrc = os.path.join(ROOT, "paper_2507_02620_b200", "csrc")
+    subprocess.run([nvcc, "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-I", csrc, "-I",
+                    os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True, capture_output=True)
+    rec, sub_prefix, sub_in, dec_in = map(int, subprocess.run([str(exe)], check=True, capture_output=True,
+                                                              text=True).stdout.split())
+    assert bench.D2H_TICK == rec
+    assert bench.H2D_SUBMIT == sub_in
+    assert bench.H2D_PRUNE == dec_in
+    assert 4 * (14 + 2 * 512) == sub_prefix   # the synchronous submit's read-back (bench comment)
