@@ -905,7 +905,8 @@ int launch_attention(fs_ctx* c, int l) {
     } else {
     if ((QR == 128 || QR == 256) && hd == ATT_HD && !getenv("FS_NO_TC_ATTN")) {
       // grouped-query rows fill 128-row M-tiles: tcgen05 attention, one CTA per SM
-      const int nsplit = std::max(1, std::min(c->n_sms / Hkv, c->att_chunk_cap * 4));
+      int nsplit = std::max(1, std::min(c->n_sms / Hkv, c->att_chunk_cap * 4));
+      if (getenv("FS_GQA_NSPLIT")) nsplit = std::max(1, std::min(c->att_chunk_cap * 4, atoi(getenv("FS_GQA_NSPLIT"))));
       TcAttnArgs ta;
       ta.a = a;
       cudaLaunchConfig_t lc = {};
