@@ -27,6 +27,12 @@
 #ifndef FS_TCA_SPLITROW
 #define FS_TCA_SPLITROW 1
 #endif
+// 1: the split-row softmax computes its scaled scores, row sums and hi/lo
+// residuals with Blackwell's packed FP32 instructions (FFMA2 / FADD2: two lanes
+// per instruction, each lane an IEEE fma / add with round-to-nearest)
+#ifndef FS_TCA_F32X2
+#define FS_TCA_F32X2 1
+#endif
 // 1: QK^T(j+1) of an M-tile is issued right after P.V(j), relying on the
 // in-order execution of one thread's tcgen05.mma for the P (read by P.V) that
 // QK^T overwrites; 0: wait for P.V(j) to complete first
@@ -112,6 +118,24 @@ FS_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::c
 // P formats of the P.V MMA: bf16, bf16 hi + lo pair (two MMAs), fp16 (A f16
 // from TMEM with B = V bf16 in the same kind::f16 instruction)
 constexpr int TCA_P_BF16 = 0, TCA_P_HILO = 1, TCA_P_F16 = 2;
+
+// packed FP32 pairs (sm_100a): {lo lane, hi lane} in one 64-bit register pair
+FS_DEV uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+FS_DEV void f2_unpack(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+FS_DEV uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+FS_DEV uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 template <int MT2, int PF>
 __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
@@ -480,6 +504,38 @@ __global__ void __launch_bounds__(TcAttnCfg<MT2>::THREADS, 1)
       if (need_mask)
 #pragma unroll
         for (int c = 0; c < 4; c++) mask16(sv + c * 16, key0 + c * 16);
+#if FS_TCA_F32X2
+      if constexpr (PF != TCA_P_F16) {
+        // p = 2^(s*c - M*c) two scores per FFMA2, row sums in two packed
+        // accumulators, P_lo = p - float(P_hi) two per FFMA2 (h * -1 + p: exact product)
+        const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(nm, nm), m12 = f2_pack(-1.f, -1.f);
+        uint64_t acc2[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+#pragma unroll
+        for (int c16 = 0; c16 < 4; c16++) {
+          uint32_t pk[8], pl[8];
+#pragma unroll
+          for (int i = 0; i < 8; i++) {
+            const int k0 = c16 * 16 + 2 * i;
+            float t0, t1;
+            f2_unpack(f2_fma(f2_pack(sv[k0], sv[k0 + 1]), sc2, nm2), t0, t1);
+            const float x0 = ex2_approx(t0), x1 = ex2_approx(t1);
+            const uint64_t x2 = f2_pack(x0, x1);
+            acc2[i & 1] = f2_add(acc2[i & 1], x2);
+            const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+            const uint32_t u = *reinterpret_cast<const uint32_t*>(&hb);
+            pk[i] = u;
+            if constexpr (PLO) {
+              float l0, l1;
+              f2_unpack(f2_fma(f2_pack(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u)), m12, x2), l0, l1);
+              pl[i] = pack_bf16(l0, l1);
+            }
+          }
+          tmem_st8(tS + c16 * 8, pk);
+          if constexpr (PLO) tmem_st8(tS + 32 + c16 * 8, pl);
+        }
+        f2_unpack(f2_add(acc2[0], acc2[1]), ls[0], ls[1]);
+      } else
+#endif
 #pragma unroll
       for (int c16 = 0; c16 < 4; c16++) {
         uint32_t pk[8], pl[8];
